@@ -1,0 +1,842 @@
+// lmg.cu -- C-ABI + stream-ordered orchestration of the layer-parallel FAS solver (sm_100a).
+//
+// Every reference numeric routine on the hot path maps onto launches of one FP64-DMMA step
+// kernel (lmg_gemm.cuh) with a fused epilogue, plus a few HBM-bound elementwise kernels:
+//
+//   fused FCF sweep        multigrid.py:160-172   2c launches, each one step of every block
+//   C-row residual (P)     multigrid.py:208       1 extra step of the same sweep
+//   coarse source + inject multigrid.py:209-212   1 launch (E_COARSE) + row 0
+//   coarsest solve         multigrid.py:214-215   n_coarse-1 single-task launches
+//   correction             multigrid.py:227       1 elementwise launch
+//   post-correction norm   multigrid.py:228       2 launches on rows {kc, kc+1} + reduction
+//
+// Residual rows that are algebraically zero (F rows after FCF; all but {kc, kc+1} after the
+// correction) are exactly 0.0 in the reference because the same propagate_values recomputes
+// them (multigrid.py:118-119); they are skipped here and contribute exactly 0.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lmg.h"
+#include "lmg_gemm.cuh"
+
+using namespace lmg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& m) {
+  g_err = m;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                              \
+  do {                                                                           \
+    cudaError_t e_ = (x);                                                        \
+    if (e_ != cudaSuccess)                                                       \
+      return fail(LMG_ERR_CUDA, std::string(#x ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TRY(x)                  \
+  do {                          \
+    int r_ = (x);               \
+    if (r_ != LMG_OK) return r_; \
+  } while (0)
+
+inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------------------------------
+// elementwise kernels (HBM-bound; grid-stride, 2 doubles per thread-iteration where possible)
+
+__global__ void k_copy_rows(double* __restrict__ dst, int64_t dst_ts, const double* __restrict__ src,
+                            int64_t src_ts, int64_t nrows, int64_t len) {
+  const int64_t total = nrows * len;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / len, i = e - r * len;
+    dst[r * dst_ts + i] = src[r * src_ts + i];
+  }
+}
+
+// multigrid.py:227  states[::c] += solved - coarse_states   (coarse_states == states[::c] bitwise)
+__global__ void k_correct(double* __restrict__ U, int64_t u_ts, const double* __restrict__ V,
+                          int64_t v_ts, int64_t nrows, int64_t len) {
+  const int64_t total = nrows * len;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = e / len, i = e - r * len;
+    double u = U[r * u_ts + i];
+    U[r * u_ts + i] = __dadd_rn(u, __dadd_rn(V[r * v_ts + i], -u));
+  }
+}
+
+__global__ void k_add(double* __restrict__ out, const double* __restrict__ a,
+                      const double* __restrict__ b, int64_t len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __dadd_rn(a[i], b[i]);
+}
+
+// row 0 of the coarse source: S_H[0] = U_H[0] + (f[0] - U[0])  (propagation_operator row 0 +
+// residual row 0, multigrid.py:124,142); optionally V[0] = U[0] (the copy the recursion edits)
+__global__ void k_row0_coarse(const double* __restrict__ U0, const double* __restrict__ S0,
+                              double* __restrict__ SH0, double* __restrict__ V0, int64_t len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double u = U0[i];
+    SH0[i] = __dadd_rn(u, __dadd_rn(S0[i], -u));
+    if (V0) V0[i] = u;
+  }
+}
+
+// residual row 0: r = f[0] - u[0] (multigrid.py:124) + per-sample partial sum of squares
+__global__ void k_resid_row0(const double* __restrict__ S0, const double* __restrict__ U0,
+                             double* __restrict__ R0, double* __restrict__ part, int64_t slot,
+                             int B, int q) {
+  __shared__ double sh[256];
+  const int b = blockIdx.x;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    int64_t idx = (int64_t)b * q + i;
+    double r = U0 ? __dadd_rn(S0[idx], -U0[idx]) : S0[idx];
+    if (R0) R0[idx] = r;
+    acc = fma(r, r, acc);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && part) part[slot * B + b] = sh[0];
+}
+
+// norms[b] = sqrt(sum over slots, in slot order) -- deterministic for any launch geometry
+__global__ void k_reduce_norms(const double* __restrict__ part, int64_t nslots, int B,
+                               double* __restrict__ norms) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double s = 0.0;
+  for (int64_t k = 0; k < nslots; ++k) s += part[k * B + b];
+  norms[b] = sqrt(s);
+}
+
+// bias gradient + SGD: gb_n[i] = (h * sum_b lam^{n+1}[b,i] D_n[b,i]) * scale ; b_n -= lr*gb_n
+__global__ void k_bias_grads(const double* __restrict__ lam_top, int64_t lam_ts,
+                             const double* __restrict__ D, int N, int B, int q, double h,
+                             double scale, double lr, double* __restrict__ gb,
+                             double* __restrict__ bias, int64_t b_stride) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)N * q) return;
+  int n = (int)(e / q), i = (int)(e - (int64_t)n * q);
+  const double* L = lam_top + (int64_t)n * lam_ts;
+  const double* Dn = D + (int64_t)n * B * q;
+  double s = 0.0;
+  for (int b = 0; b < B; ++b) s += __dmul_rn(L[(int64_t)b * q + i], Dn[(int64_t)b * q + i]);
+  double g = __dmul_rn(__dmul_rn(s, h), scale);
+  if (gb) gb[e] = g;
+  if (lr != 0.0 && bias) {
+    double* bp = bias + (int64_t)n * b_stride + i;
+    *bp = __dadd_rn(*bp, -__dmul_rn(lr, g));
+  }
+}
+
+int grid_for(int64_t total) {
+  int64_t g = (total + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+int copy_rows(double* dst, int64_t dst_ts, const double* src, int64_t src_ts, int64_t nrows,
+              int64_t len, cudaStream_t st) {
+  if (nrows <= 0 || len <= 0) return LMG_OK;
+  k_copy_rows<<<grid_for(nrows * len), 256, 0, st>>>(dst, dst_ts, src, src_ts, nrows, len);
+  CUDA_TRY(cudaGetLastError());
+  return LMG_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// step-GEMM dispatch
+
+enum Layout { L_FWD = 0, L_ADJ = 1, L_PG = 2 };
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BKM, bool ASC, int VEC>
+int launch_cfg(const StepArgs& a, cudaStream_t st) {
+  using C = GemmCfg<BM, BN, BK, WM, WN, ST, AK, BKM, ASC>;
+  auto kern = step_gemm<BM, BN, BK, WM, WN, ST, AK, BKM, ASC, VEC>;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.ntasks);
+  kern<<<grid, C::NTHREADS, C::SMEM, st>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return LMG_OK;
+}
+
+constexpr int TBM = 64, TBN = 64, TBK = 16, TWM = 2, TWN = 2, TST = 4;
+
+int n_tiles(int N) { return (N + TBN - 1) / TBN; }
+
+bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int launch_step(Layout L, const StepArgs& a, cudaStream_t st) {
+  if (a.ntasks <= 0 || a.M <= 0 || a.N <= 0) return LMG_OK;
+  if (a.ntasks > 65535) return fail(LMG_ERR_CONFIGURATION, "too many tasks in one launch");
+  bool v2 = (a.lda % 2 == 0) && (a.ldb % 2 == 0) && aligned16(a.A) && aligned16(a.Bm) &&
+            aligned16(a.Ds) && (a.A_ts % 2 == 0) && (a.B_ts % 2 == 0) && (a.Ds_ts % 2 == 0);
+  if (L == L_FWD) v2 = v2 && (a.K % 2 == 0);
+  if (L == L_ADJ) v2 = v2 && (a.K % 2 == 0) && (a.N % 2 == 0);
+  if (L == L_PG) v2 = v2 && (a.M % 2 == 0) && (a.N % 2 == 0);
+  switch (L) {
+    case L_FWD:
+      return v2 ? launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, true, true, false, 2>(a, st)
+                : launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, true, true, false, 1>(a, st);
+    case L_ADJ:
+      return v2 ? launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, true, false, true, 2>(a, st)
+                : launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, true, false, true, 1>(a, st);
+    case L_PG:
+      return v2 ? launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, false, false, true, 2>(a, st)
+                : launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, false, false, true, 1>(a, st);
+  }
+  return fail(LMG_ERR_CONFIGURATION, "bad layout");
+}
+
+// ------------------------------------------------------------------------------------------
+// systems
+
+bool is_adjoint(const lmg_system& s) { return s.kind == LMG_DENSE_ADJOINT || s.kind == LMG_CONV_ADJOINT; }
+
+int check_sys(const lmg_system* s, int B) {
+  if (!s) return fail(LMG_ERR_CONFIGURATION, "null system");
+  if (s->num_layers < 1) return fail(LMG_ERR_CONFIGURATION, "a system needs at least one block");
+  if (s->width < 1 || B < 1) return fail(LMG_ERR_DIMENSION, "width and batch must be >= 1");
+  if (s->kind == LMG_CONV || s->kind == LMG_CONV_ADJOINT)
+    return fail(LMG_ERR_CONFIGURATION, "conv2d systems are not supported by this build yet");
+  if (s->kind != LMG_DENSE && s->kind != LMG_DENSE_ADJOINT)
+    return fail(LMG_ERR_CONFIGURATION, "unknown system kind");
+  if (s->act < 0 || s->act > 2) return fail(LMG_ERR_CONFIGURATION, "unknown activation");
+  if (!s->W) return fail(LMG_ERR_CONFIGURATION, "null weights");
+  if (is_adjoint(*s) && !s->D) return fail(LMG_ERR_CONFIGURATION, "adjoint system without D");
+  if (!(std::isfinite(s->step)) || s->step < 0.0)
+    return fail(LMG_ERR_CONFIGURATION, "step_size must be finite and >= 0");
+  return LMG_OK;
+}
+
+lmg_system coarsen(const lmg_system& s, int c) {
+  lmg_system r = s;
+  r.num_layers = s.num_layers / c;
+  r.step = s.step * c;  // multigrid.py:101 fine.step_size * coarsening, level by level
+  r.w_stride = s.w_stride * c;
+  r.b_stride = s.b_stride * c;
+  r.d_stride = s.d_stride * c;
+  return r;
+}
+
+// One launch of the layer step on `ntasks` blocks blk0, blk0+blk_step, ...: task t reads its input
+// state at x + t*x_ts and writes according to `epi`.
+struct Fam {
+  int ntasks = 0, blk0 = 0, blk_step = 1;
+  const double* x = nullptr; int64_t x_ts = 0;
+  const double* s = nullptr; int64_t s_ts = 0;
+  const double* y = nullptr; int64_t y_ts = 0;
+  const double* p = nullptr; int64_t p_ts = 0;
+  double* out = nullptr; int64_t out_ts = 0;
+  double* out2 = nullptr; int64_t out2_ts = 0;
+  double* part = nullptr; int64_t slot0 = 0;
+};
+
+int family(const lmg_system& S, int B, int epi, const Fam& f, cudaStream_t st) {
+  if (f.ntasks <= 0) return LMG_OK;
+  const int q = S.width;
+  StepArgs a{};
+  a.M = B; a.N = q; a.K = q; a.ntasks = f.ntasks;
+  a.epi = epi; a.h = S.step; a.lr = 0.0; a.scale = 1.0;
+  a.A = f.x; a.A_ts = f.x_ts; a.lda = q;
+  a.Bm = S.W + (int64_t)f.blk0 * S.w_stride; a.B_ts = (int64_t)f.blk_step * S.w_stride; a.ldb = q;
+  a.x = f.x; a.x_ts = f.x_ts;
+  a.s = f.s; a.s_ts = f.s_ts;
+  a.y = f.y; a.y_ts = f.y_ts;
+  a.p = f.p; a.p_ts = f.p_ts;
+  a.out = f.out; a.out_ts = f.out_ts;
+  a.out2 = f.out2; a.out2_ts = f.out2_ts;
+  a.ldc = q;
+  a.part = f.part; a.part_slot0 = f.slot0; a.part_ld = B;
+  if (is_adjoint(S)) {
+    a.act = LMG_ACT_IDENTITY;
+    a.bias = nullptr;
+    a.Ds = S.D + (int64_t)f.blk0 * S.d_stride; a.Ds_ts = (int64_t)f.blk_step * S.d_stride;
+    return launch_step(L_ADJ, a, st);
+  }
+  a.act = S.act;
+  a.bias = S.b ? S.b + (int64_t)f.blk0 * S.b_stride : nullptr;
+  a.bias_ts = (int64_t)f.blk_step * S.b_stride;
+  return launch_step(L_FWD, a, st);
+}
+
+// source row pointer for row j (NULL = zero row)
+inline const double* src_row(const double* src, int mode, int64_t BQ, int j) {
+  if (!src) return nullptr;
+  if (mode == LMG_SRC_HEAD) return j == 0 ? src : nullptr;
+  return src + (int64_t)j * BQ;
+}
+// source family pointer for rows j0, j0+step, ... (all >= 1 in head mode -> NULL)
+inline const double* src_fam(const double* src, int mode, int64_t BQ, int j0) {
+  if (!src || mode == LMG_SRC_HEAD) return nullptr;
+  return src + (int64_t)j0 * BQ;
+}
+
+// ------------------------------------------------------------------------------------------
+// reference routines
+
+int seq_forward(const lmg_system& S, int B, const double* src, int mode, double* U, cudaStream_t st) {
+  const int64_t BQ = (int64_t)B * S.width;
+  TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]
+  for (int j = 1; j < S.num_layers; ++j) {
+    Fam f;
+    f.ntasks = 1; f.blk0 = j - 1;
+    f.x = U + (int64_t)(j - 1) * BQ;
+    f.s = src_row(src, mode, BQ, j);
+    f.out = U + (int64_t)j * BQ;
+    TRY(family(S, B, E_PROP, f, st));
+  }
+  return LMG_OK;
+}
+
+// F-sweep step i (1..c-1) of every block k: row kc+i from row kc+i-1
+int f_step(const lmg_system& S, int B, int c, double* U, const double* src, int mode, int i,
+           int k_first, cudaStream_t st) {
+  const int64_t BQ = (int64_t)B * S.width;
+  const int nb = S.num_layers / c;
+  Fam f;
+  f.ntasks = nb - k_first; f.blk0 = k_first * c + i - 1; f.blk_step = c;
+  f.x = U + (int64_t)(k_first * c + i - 1) * BQ; f.x_ts = c * BQ;
+  f.s = src_fam(src, mode, BQ, k_first * c + i); f.s_ts = c * BQ;
+  f.out = U + (int64_t)(k_first * c + i) * BQ; f.out_ts = c * BQ;
+  return family(S, B, E_PROP, f, st);
+}
+
+int f_relax(const lmg_system& S, int B, int c, double* U, const double* src, int mode, cudaStream_t st) {
+  for (int i = 1; i < c; ++i) TRY(f_step(S, B, c, U, src, mode, i, 0, st));
+  return LMG_OK;
+}
+
+// C-sweep: rows kc (k >= 1) from rows kc-1 (pre-sweep values), states[0] = source[0]
+int c_step(const lmg_system& S, int B, int c, double* U, const double* src, int mode,
+           double* out, int64_t out_ts, cudaStream_t st) {
+  const int64_t BQ = (int64_t)B * S.width;
+  const int nb = S.num_layers / c;
+  Fam f;
+  f.ntasks = nb - 1; f.blk0 = c - 1; f.blk_step = c;
+  f.x = U + (int64_t)(c - 1) * BQ; f.x_ts = c * BQ;
+  f.s = src_fam(src, mode, BQ, c); f.s_ts = c * BQ;
+  f.out = out; f.out_ts = out_ts;
+  return family(S, B, E_PROP, f, st);
+}
+
+int c_relax(const lmg_system& S, int B, int c, double* U, const double* src, int mode, cudaStream_t st) {
+  const int64_t BQ = (int64_t)B * S.width;
+  TRY(c_step(S, B, c, U, src, mode, U + (int64_t)c * BQ, c * BQ, st));
+  return copy_rows(U, 0, src, 0, 1, BQ, st);
+}
+
+// Fused FCF (bitwise identical to F, C, F): launch s = 0..c-2 runs block k-1's first F step s+1
+// for every k >= 1 (writing the block's F rows, which the reference also does), s = c-1 the C
+// step, s = c..2c-2 the second F sweep.  Each C row's old value is consumed at s = 0, before the
+// C step overwrites it at s = c-1, and block nb-1's first F sweep (dead in the reference) is
+// skipped.  If P != NULL a final step writes P[k+1] = propagate(U[(k+1)c-1]) for k < nb-1: the
+// propagated value of every interior C row, i.e. the C-row residual R[kc] = P[k] - U[kc].
+int fcf(const lmg_system& S, int B, int c, double* U, const double* src, int mode, double* P,
+        cudaStream_t st) {
+  const int64_t BQ = (int64_t)B * S.width;
+  const int nb = S.num_layers / c;
+  for (int s = 0; s + 1 < c; ++s) {  // first F sweep of blocks 0..nb-2
+    Fam f;
+    f.ntasks = nb - 1; f.blk0 = s; f.blk_step = c;
+    f.x = U + (int64_t)s * BQ; f.x_ts = c * BQ;
+    f.s = src_fam(src, mode, BQ, s + 1); f.s_ts = c * BQ;
+    f.out = U + (int64_t)(s + 1) * BQ; f.out_ts = c * BQ;
+    TRY(family(S, B, E_PROP, f, st));
+  }
+  TRY(c_step(S, B, c, U, src, mode, U + (int64_t)c * BQ, c * BQ, st));
+  TRY(copy_rows(U, 0, src, 0, 1, BQ, st));
+  TRY(f_relax(S, B, c, U, src, mode, st));
+  if (P) TRY(c_step(S, B, c, U, src, mode, P + BQ, BQ, st));
+  return LMG_OK;
+}
+
+// full residual (all rows) -> optional R, per-sample partials from slot 0
+int residual_full(const lmg_system& S, int B, const double* U, const double* src, int mode,
+                  double* R, double* part, cudaStream_t st, int64_t* nslots) {
+  const int q = S.width;
+  const int64_t BQ = (int64_t)B * q;
+  const int n = S.num_layers;
+  k_resid_row0<<<B, 256, 0, st>>>(src, U, R, part, 0, B, q);
+  CUDA_TRY(cudaGetLastError());
+  Fam f;
+  f.ntasks = n - 1; f.blk0 = 0; f.blk_step = 1;
+  f.x = U; f.x_ts = BQ;
+  f.s = src_fam(src, mode, BQ, 1); f.s_ts = BQ;
+  f.y = U + BQ; f.y_ts = BQ;
+  f.out = R ? R + BQ : nullptr; f.out_ts = BQ;
+  f.part = part; f.slot0 = 1;
+  TRY(family(S, B, E_RESID, f, st));
+  *nslots = 1 + (int64_t)(n - 1) * n_tiles(q);
+  return LMG_OK;
+}
+
+// residual after the C correction: only rows {kc, kc+1} can be nonzero (plus row 0)
+int residual_post(const lmg_system& S, int B, int c, const double* U, const double* src, int mode,
+                  double* part, cudaStream_t st, int64_t* nslots) {
+  const int q = S.width;
+  const int64_t BQ = (int64_t)B * q;
+  const int nb = S.num_layers / c;
+  const int nt = n_tiles(q);
+  k_resid_row0<<<B, 256, 0, st>>>(src, U, nullptr, part, 0, B, q);
+  CUDA_TRY(cudaGetLastError());
+  Fam f1;  // rows kc, k = 1..nb-1
+  f1.ntasks = nb - 1; f1.blk0 = c - 1; f1.blk_step = c;
+  f1.x = U + (int64_t)(c - 1) * BQ; f1.x_ts = c * BQ;
+  f1.s = src_fam(src, mode, BQ, c); f1.s_ts = c * BQ;
+  f1.y = U + (int64_t)c * BQ; f1.y_ts = c * BQ;
+  f1.part = part; f1.slot0 = 1;
+  TRY(family(S, B, E_RESID, f1, st));
+  Fam f2;  // rows kc+1, k = 0..nb-1
+  f2.ntasks = nb; f2.blk0 = 0; f2.blk_step = c;
+  f2.x = U; f2.x_ts = c * BQ;
+  f2.s = src_fam(src, mode, BQ, 1); f2.s_ts = c * BQ;
+  f2.y = U + BQ; f2.y_ts = c * BQ;
+  f2.part = part; f2.slot0 = 1 + (int64_t)(nb - 1) * nt;
+  TRY(family(S, B, E_RESID, f2, st));
+  *nslots = 1 + (int64_t)(2 * nb - 1) * nt;
+  return LMG_OK;
+}
+
+int reduce_norms(const double* part, int64_t nslots, int B, double* norms, cudaStream_t st) {
+  k_reduce_norms<<<(B + 127) / 128, 128, 0, st>>>(part, nslots, B, norms);
+  CUDA_TRY(cudaGetLastError());
+  return LMG_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// hierarchy + workspace
+
+int levels_for(int n, int c, int threshold, std::vector<int>* sizes) {
+  if (c < 2) return fail(LMG_ERR_CONFIGURATION, "coarsening factor must be an integer >= 2, got " + std::to_string(c));
+  if (threshold <= 0) threshold = std::max(1, n / c);
+  sizes->clear();
+  sizes->push_back(n);
+  while (sizes->back() > threshold) {
+    if (sizes->back() % c != 0)
+      return fail(LMG_ERR_CONFIGURATION, "cannot coarsen " + std::to_string(sizes->back()) +
+                                             " layers by factor " + std::to_string(c));
+    sizes->push_back(sizes->back() / c);
+  }
+  return LMG_OK;
+}
+
+struct Workspace {
+  std::vector<double*> P, SH, V;  // per relaxed level l: P[l]; per coarse level l+1: SH, V
+  double* part = nullptr;
+  double* norms = nullptr;
+  size_t bytes = 0;
+};
+
+size_t part_slots(int n, int q) { return 1 + (size_t)n * (size_t)n_tiles(q); }
+
+int layout_ws(const lmg_system& fine, int nlevels, int c, int B, char* base, Workspace* ws) {
+  const int64_t BQ = (int64_t)B * fine.width;
+  size_t off = 0;
+  auto take = [&](size_t doubles) {
+    double* p = base ? reinterpret_cast<double*>(base + off) : nullptr;
+    off += ((doubles * sizeof(double) + 255) / 256) * 256;
+    return p;
+  };
+  ws->P.assign(nlevels, nullptr);
+  ws->SH.assign(nlevels, nullptr);
+  ws->V.assign(nlevels, nullptr);
+  int n = fine.num_layers;
+  for (int l = 0; l + 1 < nlevels; ++l) {
+    int nb = n / c;
+    ws->P[l] = take((size_t)nb * BQ);
+    ws->SH[l + 1] = take((size_t)nb * BQ);
+    ws->V[l + 1] = take((size_t)nb * BQ);
+    n = nb;
+  }
+  ws->part = take(part_slots(fine.num_layers, fine.width) * (size_t)B);
+  ws->norms = take((size_t)B);
+  ws->bytes = off;
+  return LMG_OK;
+}
+
+// multigrid.py:175-228.  `want_norm` only at the finest level: the recursive call's return value
+// is discarded by the reference (multigrid.py:218-226).
+int cycle(const lmg_system& S, int nlevels, int l, int c, int B, double* U, const double* src,
+          int mode, const Workspace& ws, bool want_norm, double* norms, cudaStream_t st) {
+  const int64_t BQ = (int64_t)B * S.width;
+  int64_t nslots = 0;
+  if (l == nlevels - 1) {  // single-level hierarchy: exact solve
+    TRY(seq_forward(S, B, src, mode, U, st));
+    if (want_norm) {
+      TRY(residual_full(S, B, U, src, mode, nullptr, ws.part, st, &nslots));
+      TRY(reduce_norms(ws.part, nslots, B, norms, st));
+    }
+    return LMG_OK;
+  }
+  const int nb = S.num_layers / c;
+  TRY(fcf(S, B, c, U, src, mode, ws.P[l], st));
+  const lmg_system Sc = coarsen(S, c);
+  const bool coarsest = (l + 1 == nlevels - 1);
+  double* SH = ws.SH[l + 1];
+  double* V = ws.V[l + 1];
+  {  // coarse FAS source S_H = L_H(U_H) + R_H, fused with the injection copy V = U[::c]
+    Fam f;
+    f.ntasks = nb - 1; f.blk0 = 0; f.blk_step = 1;  // coarse block n-1 == fine block (n-1)c
+    f.x = U; f.x_ts = c * BQ;
+    f.y = U + (int64_t)c * BQ; f.y_ts = c * BQ;
+    f.p = ws.P[l] + BQ; f.p_ts = BQ;
+    f.out = SH + BQ; f.out_ts = BQ;
+    f.out2 = coarsest ? nullptr : V + BQ; f.out2_ts = BQ;
+    TRY(family(Sc, B, E_COARSE, f, st));
+    k_row0_coarse<<<grid_for(BQ), 256, 0, st>>>(U, src, SH, coarsest ? nullptr : V, BQ);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (coarsest)
+    TRY(seq_forward(Sc, B, SH, LMG_SRC_DENSE, V, st));
+  else
+    TRY(cycle(Sc, nlevels, l + 1, c, B, V, SH, LMG_SRC_DENSE, ws, false, nullptr, st));
+  k_correct<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, c * BQ, V, BQ, nb, BQ);
+  CUDA_TRY(cudaGetLastError());
+  if (want_norm) {
+    TRY(residual_post(S, B, c, U, src, mode, ws.part, st, &nslots));
+    TRY(reduce_norms(ws.part, nslots, B, norms, st));
+  }
+  return LMG_OK;
+}
+
+int check_levels(const lmg_system& fine, int nlevels, int c) {
+  if (c < 2) return fail(LMG_ERR_CONFIGURATION, "coarsening factor must be an integer >= 2");
+  if (nlevels < 1) return fail(LMG_ERR_CONFIGURATION, "need at least one level");
+  int n = fine.num_layers;
+  for (int l = 0; l + 1 < nlevels; ++l) {
+    if (n % c) return fail(LMG_ERR_CONFIGURATION, "cannot coarsen " + std::to_string(n) + " layers by factor " + std::to_string(c));
+    n /= c;
+  }
+  return LMG_OK;
+}
+
+}  // namespace
+
+// ============================================================================================
+// C-ABI
+
+extern "C" {
+
+int lmg_abi_version(void) { return 1; }
+
+const char* lmg_last_error(void) { return g_err.c_str(); }
+
+int lmg_propagate(const lmg_system* sys, int B, const double* u_start, const double* src,
+                  int src_mode, int start, int stop, double* out, void* stream) {
+  TRY(check_sys(sys, B));
+  if (start < 1 || stop < start || stop - 1 > sys->num_layers)
+    return fail(LMG_ERR_DIMENSION, "propagate range out of bounds");
+  const int64_t BQ = (int64_t)B * sys->width;
+  for (int j = start; j < stop; ++j) {
+    Fam f;
+    f.ntasks = 1; f.blk0 = j - 1;
+    f.x = j == start ? u_start : out + (int64_t)(j - 1 - start) * BQ;
+    f.s = src_row(src, src_mode, BQ, j);
+    f.out = out + (int64_t)(j - start) * BQ;
+    TRY(family(*sys, B, E_PROP, f, S_(stream)));
+  }
+  return LMG_OK;
+}
+
+int lmg_sequential_forward(const lmg_system* sys, int B, const double* src, int src_mode,
+                           double* states, void* stream) {
+  TRY(check_sys(sys, B));
+  return seq_forward(*sys, B, src, src_mode, states, S_(stream));
+}
+
+int lmg_propagation_operator(const lmg_system* sys, int B, const double* states, double* out,
+                             void* stream) {
+  TRY(check_sys(sys, B));
+  const int64_t BQ = (int64_t)B * sys->width;
+  TRY(copy_rows(out, 0, states, 0, 1, BQ, S_(stream)));
+  Fam f;
+  f.ntasks = sys->num_layers - 1;
+  f.x = states; f.x_ts = BQ;
+  f.y = states + BQ; f.y_ts = BQ;
+  f.out = out + BQ; f.out_ts = BQ;
+  return family(*sys, B, E_PROPOP, f, S_(stream));
+}
+
+size_t lmg_residual_workspace(const lmg_system* sys, int B) {
+  if (!sys) return 0;
+  return (part_slots(sys->num_layers, sys->width) * (size_t)B) * sizeof(double) + 256;
+}
+
+int lmg_compute_residual(const lmg_system* sys, int B, const double* states, const double* src,
+                         int src_mode, double* out, double* norms, void* work, void* stream) {
+  TRY(check_sys(sys, B));
+  if (norms && !work) return fail(LMG_ERR_CONFIGURATION, "norms requested without workspace");
+  int64_t nslots = 0;
+  double* part = norms ? reinterpret_cast<double*>(work) : nullptr;
+  TRY(residual_full(*sys, B, states, src, src_mode, out, part, S_(stream), &nslots));
+  if (norms) TRY(reduce_norms(part, nslots, B, norms, S_(stream)));
+  return LMG_OK;
+}
+
+int lmg_restrict(const double* fine, int n, int B, int q, int c, double* out, void* stream) {
+  if (c < 1 || n % c) return fail(LMG_ERR_DIMENSION, "cannot restrict " + std::to_string(n) + " rows by factor " + std::to_string(c));
+  const int64_t BQ = (int64_t)B * q;
+  return copy_rows(out, BQ, fine, c * BQ, n / c, BQ, S_(stream));
+}
+
+int lmg_assemble_coarse_source(const lmg_system* coarse, int B, const double* UH,
+                               const double* RH, double* out, void* stream) {
+  TRY(check_sys(coarse, B));
+  const int64_t BQ = (int64_t)B * coarse->width;
+  // row 0: propagation_operator row 0 (U_H[0]) plus the residual row 0
+  k_add<<<grid_for(BQ), 256, 0, S_(stream)>>>(out, UH, RH, BQ);
+  CUDA_TRY(cudaGetLastError());
+  Fam f;
+  f.ntasks = coarse->num_layers - 1;
+  f.x = UH; f.x_ts = BQ;
+  f.y = UH + BQ; f.y_ts = BQ;
+  f.p = RH + BQ; f.p_ts = BQ;
+  f.out = out + BQ; f.out_ts = BQ;
+  return family(*coarse, B, E_COARSE_R, f, S_(stream));
+}
+
+int lmg_f_relax(const lmg_system* sys, int B, int c, double* states, const double* src,
+                int src_mode, void* stream) {
+  TRY(check_sys(sys, B));
+  TRY(check_levels(*sys, 2, c));
+  return f_relax(*sys, B, c, states, src, src_mode, S_(stream));
+}
+
+int lmg_c_relax(const lmg_system* sys, int B, int c, double* states, const double* src,
+                int src_mode, void* stream) {
+  TRY(check_sys(sys, B));
+  TRY(check_levels(*sys, 2, c));
+  return c_relax(*sys, B, c, states, src, src_mode, S_(stream));
+}
+
+int lmg_fcf_relax(const lmg_system* sys, int B, int c, double* states, const double* src,
+                  int src_mode, void* stream) {
+  TRY(check_sys(sys, B));
+  TRY(check_levels(*sys, 2, c));
+  return fcf(*sys, B, c, states, src, src_mode, nullptr, S_(stream));
+}
+
+int lmg_num_levels(int n, int c, int threshold, int* levels_out) {
+  std::vector<int> sizes;
+  TRY(levels_for(n, c, threshold, &sizes));
+  if (levels_out) *levels_out = (int)sizes.size();
+  return LMG_OK;
+}
+
+size_t lmg_solver_workspace(const lmg_system* fine, int nlevels, int c, int B) {
+  if (!fine || nlevels < 1 || c < 2) return 0;
+  Workspace ws;
+  layout_ws(*fine, nlevels, c, B, nullptr, &ws);
+  return ws.bytes;
+}
+
+int lmg_mg_cycle(const lmg_system* fine, int nlevels, int c, int B, double* states,
+                 const double* src, int src_mode, double* norms, void* work, size_t work_bytes,
+                 void* stream) {
+  TRY(check_sys(fine, B));
+  TRY(check_levels(*fine, nlevels, c));
+  Workspace ws;
+  layout_ws(*fine, nlevels, c, B, reinterpret_cast<char*>(work), &ws);
+  if (work_bytes < ws.bytes) return fail(LMG_ERR_CONFIGURATION, "workspace too small");
+  return cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, norms != nullptr,
+               norms ? norms : ws.norms, S_(stream));
+}
+
+int lmg_solve(const lmg_system* fine, int nlevels, int c, int B, double* states,
+              const double* src, int src_mode, int use_initial, double tol, int max_cycles,
+              double* hist_host, int32_t* cycles_host, int32_t* converged_host, void* work,
+              size_t work_bytes, void* stream) {
+  TRY(check_sys(fine, B));
+  if (!(std::isfinite(tol) && tol > 0))
+    return fail(LMG_ERR_CONFIGURATION, "tolerance must be a finite positive number");
+  if (max_cycles < 1) return fail(LMG_ERR_CONFIGURATION, "max_cycles must be >= 1");
+  TRY(check_levels(*fine, nlevels, c));
+  cudaStream_t st = S_(stream);
+  Workspace ws;
+  layout_ws(*fine, nlevels, c, B, reinterpret_cast<char*>(work), &ws);
+  if (work_bytes < ws.bytes) return fail(LMG_ERR_CONFIGURATION, "workspace too small");
+  const int n = fine->num_layers, q = fine->width;
+  const int64_t BQ = (int64_t)B * q;
+
+  if (!use_initial) TRY(copy_rows(states, BQ, src, 0, n, BQ, st));  // initial_guess: tile(f[0])
+  int64_t nslots = 0;
+  TRY(residual_full(*fine, B, states, src, src_mode, nullptr, ws.part, st, &nslots));
+  TRY(reduce_norms(ws.part, nslots, B, ws.norms, st));
+
+  std::vector<double> nrm(B);
+  CUDA_TRY(cudaMemcpyAsync(nrm.data(), ws.norms, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<int> done(B, 0);
+  int ndone = 0;
+  for (int b = 0; b < B; ++b) {
+    hist_host[b] = nrm[b];
+    cycles_host[b] = 0;
+    if (nrm[b] <= tol) { done[b] = 1; ++ndone; }
+  }
+  // samples that stop while others continue are parked here (multigrid.py:297 per sample)
+  std::vector<std::pair<int, double*>> parked;
+  auto park = [&](int b) -> int {
+    double* buf = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&buf), (size_t)n * q * sizeof(double), st));
+    TRY(copy_rows(buf, q, states + (int64_t)b * q, BQ, n, q, st));
+    parked.emplace_back(b, buf);
+    return LMG_OK;
+  };
+  for (int b = 0; b < B && ndone < B; ++b)
+    if (done[b]) TRY(park(b));
+
+  int cyc = 0;
+  while (ndone < B && cyc < max_cycles) {
+    TRY(cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st));
+    ++cyc;
+    CUDA_TRY(cudaMemcpyAsync(nrm.data(), ws.norms, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int newly = 0;
+    for (int b = 0; b < B; ++b) {
+      if (done[b]) continue;
+      hist_host[(int64_t)cyc * B + b] = nrm[b];
+      cycles_host[b] = cyc;
+      if (nrm[b] <= tol) { done[b] = 1; ++newly; }
+    }
+    ndone += newly;
+    if (newly && ndone < B)
+      for (int b = 0; b < B; ++b)
+        if (done[b] && std::none_of(parked.begin(), parked.end(), [&](auto& pb) { return pb.first == b; }))
+          TRY(park(b));
+  }
+  for (auto& pb : parked) {
+    TRY(copy_rows(states + (int64_t)pb.first * q, BQ, pb.second, q, n, q, st));
+    CUDA_TRY(cudaFreeAsync(pb.second, st));
+  }
+  for (int b = 0; b < B; ++b) converged_host[b] = done[b];
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return LMG_OK;
+}
+
+int lmg_act_deriv(const lmg_system* fine, int B, const double* states, double* D, void* stream) {
+  TRY(check_sys(fine, B));
+  if (is_adjoint(*fine)) return fail(LMG_ERR_CONFIGURATION, "act_deriv needs a forward system");
+  const int64_t BQ = (int64_t)B * fine->width;
+  Fam f;
+  f.ntasks = fine->num_layers;
+  f.x = states; f.x_ts = BQ;
+  f.out = D; f.out_ts = BQ;
+  return family(*fine, B, E_DERIV, f, S_(stream));
+}
+
+int lmg_param_grads(const lmg_system* fine, int B, const double* states, const double* lam,
+                    const double* D, double scale, double lr, double* gW, double* gb,
+                    void* stream) {
+  TRY(check_sys(fine, B));
+  if (is_adjoint(*fine)) return fail(LMG_ERR_CONFIGURATION, "param_grads needs the forward system");
+  if (!gW && lr == 0.0 && !gb) return LMG_OK;
+  const int N = fine->num_layers, q = fine->width;
+  const int64_t BQ = (int64_t)B * q;
+  cudaStream_t st = S_(stream);
+  StepArgs a{};
+  a.M = q; a.N = q; a.K = B; a.ntasks = N;
+  a.epi = E_PGRAD; a.act = LMG_ACT_IDENTITY; a.h = fine->step; a.lr = lr; a.scale = scale;
+  a.A = lam + (int64_t)(N - 1) * BQ; a.A_ts = -BQ; a.lda = q;  // lambda^{n+1} = lam[N-1-n]
+  a.Ds = D; a.Ds_ts = BQ;
+  a.Bm = states; a.B_ts = BQ; a.ldb = q;
+  a.x = fine->W; a.x_ts = fine->w_stride;
+  a.out = const_cast<double*>(fine->W); a.out_ts = fine->w_stride;
+  a.out2 = gW; a.out2_ts = (int64_t)q * q;
+  a.ldc = q;
+  TRY(launch_step(L_PG, a, st));
+  const int64_t tot = (int64_t)N * q;
+  k_bias_grads<<<(int)((tot + 255) / 256), 256, 0, st>>>(lam + (int64_t)(N - 1) * BQ, -BQ, D, N, B, q,
+                                                         fine->step, scale, lr, gb,
+                                                         const_cast<double*>(fine->b), fine->b_stride);
+  CUDA_TRY(cudaGetLastError());
+  return LMG_OK;
+}
+
+int lmg_dense_apply(const double* W, const double* b, int act, int M, int q_out, int q_in,
+                    const double* X, double* Y, void* stream) {
+  if (M < 1 || q_out < 1 || q_in < 1) return fail(LMG_ERR_DIMENSION, "empty transform");
+  if (act < 0 || act > 2) return fail(LMG_ERR_CONFIGURATION, "unknown activation");
+  StepArgs a{};
+  a.M = M; a.N = q_out; a.K = q_in; a.ntasks = 1;
+  a.epi = E_APPLY; a.act = act; a.h = 1.0; a.scale = 1.0;
+  a.A = X; a.lda = q_in;
+  a.Bm = W; a.ldb = q_in;
+  a.bias = b;
+  a.out = Y; a.ldc = q_out;
+  return launch_step(L_FWD, a, S_(stream));
+}
+
+int lmg_dense_vjp(const double* W, const double* b, int act, int M, int q_out, int q_in,
+                  const double* X, const double* G, double* gX, double* gW, double* gb,
+                  double* work, void* stream) {
+  if (M < 1 || q_out < 1 || q_in < 1) return fail(LMG_ERR_DIMENSION, "empty transform");
+  if (act < 0 || act > 2) return fail(LMG_ERR_CONFIGURATION, "unknown activation");
+  cudaStream_t st = S_(stream);
+  // work <- act'(X W^T + b)
+  StepArgs d{};
+  d.M = M; d.N = q_out; d.K = q_in; d.ntasks = 1;
+  d.epi = E_DERIV; d.act = act; d.h = 1.0; d.scale = 1.0;
+  d.A = X; d.lda = q_in; d.Bm = W; d.ldb = q_in; d.bias = b;
+  d.out = work; d.ldc = q_out;
+  TRY(launch_step(L_FWD, d, st));
+  if (gX) {  // gX = (G * D) W    (m=row, n=input feature, k=output feature)
+    StepArgs a{};
+    a.M = M; a.N = q_in; a.K = q_out; a.ntasks = 1;
+    a.epi = E_APPLY; a.act = LMG_ACT_IDENTITY; a.h = 1.0; a.scale = 1.0;
+    a.A = G; a.lda = q_out; a.Ds = work;
+    a.Bm = W; a.ldb = q_in;
+    a.out = gX; a.ldc = q_in;
+    TRY(launch_step(L_ADJ, a, st));
+  }
+  if (gW) {  // gW = sum_m (G*D)_m (x) x_m
+    StepArgs a{};
+    a.M = q_out; a.N = q_in; a.K = M; a.ntasks = 1;
+    a.epi = E_PGRAD; a.act = LMG_ACT_IDENTITY; a.h = 1.0; a.scale = 1.0; a.lr = 0.0;
+    a.A = G; a.lda = q_out; a.Ds = work;
+    a.Bm = X; a.ldb = q_in;
+    a.out2 = gW; a.ldc = q_in;
+    TRY(launch_step(L_PG, a, st));
+  }
+  if (gb) {
+    k_bias_grads<<<(q_out + 255) / 256, 256, 0, st>>>(G, 0, work, 1, M, q_out, 1.0, 1.0, 0.0, gb,
+                                                       nullptr, 0);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return LMG_OK;
+}
+
+int lmg_l2_norms(const double* x, int n, int B, int q, double* norms, void* work, void* stream) {
+  if (n < 1 || B < 1 || q < 1) return fail(LMG_ERR_DIMENSION, "empty array");
+  cudaStream_t st = S_(stream);
+  double* part = reinterpret_cast<double*>(work);
+  const int64_t BQ = (int64_t)B * q;
+  for (int j = 0; j < n; ++j) {  // one slot per row: sum_b of row j (zero source minus -x)
+    k_resid_row0<<<B, 256, 0, st>>>(x + j * BQ, nullptr, nullptr, part, j, B, q);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return reduce_norms(part, n, B, norms, st);
+}
+
+}  // extern "C"

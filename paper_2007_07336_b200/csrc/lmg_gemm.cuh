@@ -1,0 +1,295 @@
+// lmg_gemm.cuh -- FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) batched "layer step" GEMM with
+// the FAS epilogues fused in.  sm_100a.
+//
+// Why DMMA and not tcgen05: the path must run in float64 (fp32 already floors the
+// residual at 1e-6 vs tol 1e-9) and tcgen05.mma has no f64 kind.  On sm_100a the f64
+// mma.sync lowers to DMMA.8x8x4 on the FP64 tensor pipe.
+//
+// One launch evaluates `ntasks` independent layer steps ("tasks"), e.g. every block's j-th
+// F-relaxation step of a sweep.  Task t's operands are affine in t (base + t*stride), so a whole
+// sweep step is described by a handful of pointers and strides -- no device task tables.
+//
+//   C[m][n] = sum_k A(m,k) * B(k,n)          (per task)
+//   A K-major: A(m,k) = A[m*lda + k]        MN-major: A(m,k) = A[k*lda + m]
+//   B K-major: B(k,n) = B[n*ldb + k]        MN-major: B(k,n) = B[k*ldb + n]
+//   A_SCALE:   A(m,k) *= Ds(m,k)  (same layout as A) -- the adjoint's act'(pre) * lambda
+//
+// forward step   (m=b, n=i, k=k): A = U_{j-1} (B x q, K-major), B = W_j (q x q, K-major)
+// adjoint step   (m=b, n=k, k=i): A = mu * D  (K-major, scaled), B = W_j (MN-major)
+// parameter grad (m=i, n=k, k=b): A = lam * D (MN-major, scaled), B = U_j (MN-major)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lmg.h"
+
+namespace lmg {
+
+enum Epi {
+  E_PROP = 0,      // out = s + (x + h*act(pre))                       network.py:100
+  E_RESID = 1,     // r = (s + (x + h*act(pre))) - y; out=r; sum r^2   multigrid.py:124-127
+  E_COARSE = 2,    // out = (y - (x + h*act(pre))) + (p - y); out2 = y multigrid.py:142, network.py:138
+  E_COARSE_R = 3,  // out = (y - (x + h*act(pre))) + p                 multigrid.py:142
+  E_PROPOP = 4,    // out = y - (x + h*act(pre))                       network.py:138
+  E_DERIV = 5,     // out = act'(pre)                                  kernels.py:44-48
+  E_PGRAD = 6,     // g = (acc*h)*scale; out2 = g; out = x - lr*g      training.py:218-236
+  E_APPLY = 7      // out = act(pre)                                   kernels.py:139-150
+};
+
+struct StepArgs {
+  int M, N, K, ntasks;
+  int epi, act;
+  double h, lr, scale;
+  const double* A; int64_t A_ts; int lda;
+  const double* Ds; int64_t Ds_ts;
+  const double* Bm; int64_t B_ts; int ldb;
+  const double* bias; int64_t bias_ts;
+  const double* x; int64_t x_ts;
+  const double* s; int64_t s_ts;
+  const double* y; int64_t y_ts;
+  const double* p; int64_t p_ts;
+  double* out; int64_t out_ts;
+  double* out2; int64_t out2_ts;
+  int ldc;
+  double* part; int64_t part_slot0; int part_ld;
+};
+
+__device__ __forceinline__ double act_fwd(int a, double v) {
+  if (a == LMG_ACT_TANH) return tanh(v);
+  if (a == LMG_ACT_RELU) return (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(pre, 0.0)
+  return v;
+}
+
+__device__ __forceinline__ double act_der(int a, double v) {
+  if (a == LMG_ACT_TANH) {
+    double t = tanh(v);
+    return __dadd_rn(1.0, -__dmul_rn(t, t));  // 1.0 - t*t, no contraction
+  }
+  if (a == LMG_ACT_RELU) return v > 0.0 ? 1.0 : 0.0;
+  return 1.0;
+}
+
+template <int VEC>
+__device__ __forceinline__ void cp_async(double* dst, const double* src, bool ok) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  int sz = ok ? 8 * VEC : 0;
+  if (VEC == 2)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(sz));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// smem footprint (doubles) of one operand tile of T (M or N) x BK
+template <bool KMAJ, int T, int BK>
+struct TileShape {
+  static constexpr int LD = KMAJ ? (BK + 4) : (T + 4);  // +4 doubles: conflict-free fragments
+  static constexpr int SIZE = KMAJ ? T * (BK + 4) : BK * (T + 4);
+};
+
+template <bool KMAJ, int T, int BK, int VEC, int NT>
+__device__ __forceinline__ void load_tile(double* sm, const double* g, int ld, int mn0, int mnlim,
+                                          int k0, int klim, int tid) {
+  using S = TileShape<KMAJ, T, BK>;
+  if (KMAJ) {
+    constexpr int PR = BK / VEC;
+#pragma unroll
+    for (int e = tid; e < T * PR; e += NT) {
+      int r = e / PR, kk = (e % PR) * VEC;
+      int gm = mn0 + r, gk = k0 + kk;
+      bool ok = gm < mnlim && gk < klim;
+      cp_async<VEC>(sm + r * S::LD + kk, ok ? g + (int64_t)gm * ld + gk : g, ok);
+    }
+  } else {
+    constexpr int PR = T / VEC;
+#pragma unroll
+    for (int e = tid; e < BK * PR; e += NT) {
+      int kk = e / PR, r = (e % PR) * VEC;
+      int gm = mn0 + r, gk = k0 + kk;
+      bool ok = gm < mnlim && gk < klim;
+      cp_async<VEC>(sm + kk * S::LD + r, ok ? g + (int64_t)gk * ld + gm : g, ok);
+    }
+  }
+}
+
+template <bool KMAJ, int T, int BK>
+__device__ __forceinline__ double frag(const double* sm, int mn, int k) {
+  using S = TileShape<KMAJ, T, BK>;
+  return KMAJ ? sm[mn * S::LD + k] : sm[k * S::LD + mn];
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, bool ASC>
+struct GemmCfg {
+  static constexpr int NTHREADS = WM * WN * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN;  // warp tile
+  static constexpr int MT = WTM / 8, NTF = WTN / 8;   // m8n8 fragments per warp
+  static constexpr int A_SZ = TileShape<AK, BM, BK>::SIZE;
+  static constexpr int B_SZ = TileShape<BKM, BN, BK>::SIZE;
+  static constexpr int STAGE = A_SZ * (ASC ? 2 : 1) + B_SZ;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE * sizeof(double);
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, bool ASC, int VEC>
+__global__ void __launch_bounds__(WM* WN * 32)
+    step_gemm(const StepArgs a) {
+  using C = GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, ASC>;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double red[WN][BM];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  const int64_t t = blockIdx.z;
+
+  const double* A = a.A + t * a.A_ts;
+  const double* Ds = ASC ? a.Ds + t * a.Ds_ts : nullptr;
+  const double* Bm = a.Bm + t * a.B_ts;
+
+  double acc[C::MT][C::NTF][2];
+#pragma unroll
+  for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NTF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int KT = (a.K + BK - 1) / BK;
+  auto stage_ptr = [&](int s) { return smem + s * C::STAGE; };
+  auto load_stage = [&](int s, int kt) {
+    double* base = stage_ptr(s);
+    int k0 = kt * BK;
+    load_tile<AK, BM, BK, VEC, C::NTHREADS>(base, A, a.lda, m0, a.M, k0, a.K, tid);
+    if (ASC) load_tile<AK, BM, BK, VEC, C::NTHREADS>(base + C::A_SZ, Ds, a.lda, m0, a.M, k0, a.K, tid);
+    load_tile<BKM, BN, BK, VEC, C::NTHREADS>(base + C::A_SZ * (ASC ? 2 : 1), Bm, a.ldb, n0, a.N, k0,
+                                             a.K, tid);
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s, s);
+    cp_commit();
+  }
+
+  const int wm0 = wm * C::WTM, wn0 = wn * C::WTN;
+  const int fr = lane >> 2, fk = lane & 3;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      int nk = kt + STAGES - 1;
+      if (nk < KT) load_stage(nk % STAGES, nk);
+      cp_commit();
+    }
+    const double* As = stage_ptr(kt % STAGES);
+    const double* Dsm = As + C::A_SZ;
+    const double* Bs = As + C::A_SZ * (ASC ? 2 : 1);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[C::MT], bf[C::NTF];
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i) {
+        af[i] = frag<AK, BM, BK>(As, wm0 + i * 8 + fr, kk + fk);
+        if (ASC) af[i] = __dmul_rn(af[i], frag<AK, BM, BK>(Dsm, wm0 + i * 8 + fr, kk + fk));
+      }
+#pragma unroll
+      for (int j = 0; j < C::NTF; ++j) bf[j] = frag<BKM, BN, BK>(Bs, wn0 + j * 8 + fr, kk + fk);
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NTF; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_wait<0>();
+
+  // ---------------------------------------------------------------- fused epilogue
+  const int epi = a.epi, actk = a.act;
+  const double h = a.h;
+  const double* bias = a.bias ? a.bias + t * a.bias_ts : nullptr;
+  const double* X = a.x ? a.x + t * a.x_ts : nullptr;
+  const double* S = a.s ? a.s + t * a.s_ts : nullptr;
+  const double* Y = a.y ? a.y + t * a.y_ts : nullptr;
+  const double* P = a.p ? a.p + t * a.p_ts : nullptr;
+  double* O = a.out ? a.out + t * a.out_ts : nullptr;
+  double* O2 = a.out2 ? a.out2 + t * a.out2_ts : nullptr;
+  const int ldc = a.ldc;
+
+  double rowsq[C::MT];
+#pragma unroll
+  for (int i = 0; i < C::MT; ++i) {
+    rowsq[i] = 0.0;
+    const int m = m0 + wm0 + i * 8 + fr;
+#pragma unroll
+    for (int j = 0; j < C::NTF; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = n0 + wn0 + j * 8 + 2 * fk + e;
+        if (m >= a.M || n >= a.N) continue;
+        const int64_t idx = (int64_t)m * ldc + n;
+        double pre = acc[i][j][e];
+        if (bias) pre = __dadd_rn(pre, bias[n]);
+        if (epi == E_DERIV) {
+          O[idx] = act_der(actk, pre);
+          continue;
+        }
+        if (epi == E_PGRAD) {
+          double g = __dmul_rn(__dmul_rn(acc[i][j][e], h), a.scale);
+          if (O2) O2[idx] = g;
+          if (a.lr != 0.0) O[idx] = __dadd_rn(X[idx], -__dmul_rn(a.lr, g));
+          continue;
+        }
+        const double v = act_fwd(actk, pre);
+        if (epi == E_APPLY) {
+          O[idx] = v;
+          continue;
+        }
+        const double xv = X[idx];
+        const double adv = __dadd_rn(xv, __dmul_rn(h, v));  // u + h*F(u)
+        if (epi == E_PROP) {
+          O[idx] = __dadd_rn(S ? S[idx] : 0.0, adv);
+        } else if (epi == E_RESID) {
+          double r = __dadd_rn(__dadd_rn(S ? S[idx] : 0.0, adv), -Y[idx]);
+          if (O) O[idx] = r;
+          rowsq[i] = fma(r, r, rowsq[i]);
+        } else if (epi == E_COARSE) {
+          const double yv = Y[idx];
+          O[idx] = __dadd_rn(__dadd_rn(yv, -adv), __dadd_rn(P[idx], -yv));
+          if (O2) O2[idx] = yv;
+        } else if (epi == E_COARSE_R) {
+          O[idx] = __dadd_rn(__dadd_rn(Y[idx], -adv), P[idx]);
+        } else {  // E_PROPOP
+          O[idx] = __dadd_rn(Y[idx], -adv);
+        }
+      }
+    }
+  }
+  if (epi == E_RESID && a.part) {
+    // deterministic per-row partial sums: 4 lanes of a fragment row, then the WN warps
+#pragma unroll
+    for (int i = 0; i < C::MT; ++i) {
+      rowsq[i] += __shfl_xor_sync(0xffffffffu, rowsq[i], 1);
+      rowsq[i] += __shfl_xor_sync(0xffffffffu, rowsq[i], 2);
+      if (fk == 0) red[wn][wm0 + i * 8 + fr] = rowsq[i];
+    }
+    __syncthreads();
+    for (int r = tid; r < BM; r += C::NTHREADS) {
+      const int m = m0 + r;
+      if (m < a.M) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < WN; ++w) sum += red[w][r];
+        const int64_t slot = a.part_slot0 + t * gridDim.x + blockIdx.x;
+        a.part[slot * a.part_ld + m] = sum;
+      }
+    }
+  }
+}
+
+}  // namespace lmg
