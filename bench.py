@@ -1,0 +1,371 @@
+"""Benchmark: FAS forward + adjoint training step to tolerance, layer*samples/s.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+A step is one training step of BASELINE.json configs[1] -- dense tanh ResNet, 1024 layers,
+width 512, batch 256, 3-level FAS (cf 4, levels [1024, 256, 64]) -- on synthetic data from the
+reference's own seeded generators: FAS forward solve to tol 1e-9 (multigrid.py:263-311), FAS
+adjoint to tol 1e-9, per-layer parameter gradients and the SGD step (training.py:194-236).
+value = N_layers * B / seconds per step, whole job.  Inputs (theta 2 GiB, states 1 GiB) exceed
+the 126 MB L2, so no explicit flush is needed between steps.
+
+Under torchrun (--gpus N > 1) the layer axis is partitioned across ranks
+(paper_2007_07336_b200.distributed); timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1]
+    "c2": dict(depth=1024, width=512, batch=256, cf=4, threshold=64, tol=1e-9, max_cycles=50,
+               lr=0.1, workload="dense tanh ResNet 1024 layers width 512 batch 256, 3-level FAS "
+                                "(cf 4, levels [1024,256,64]) forward+adjoint training step to tol 1e-9"),
+    # configs[0]-shaped small case (CPU-runnable reference demo), for quick runs
+    "c1": dict(depth=64, width=32, batch=64, cf=4, threshold=None, tol=1e-9, max_cycles=50, lr=0.1,
+               workload="dense tanh ResNet 64 layers width 32 batch 64, 2-level FAS cf 4 "
+                        "forward+adjoint training step to tol 1e-9"),
+    # configs[4]-style HBM-bound point (q=512, B=16, cf 16)
+    "c5": dict(depth=1024, width=512, batch=16, cf=16, threshold=4, tol=1e-9, max_cycles=50, lr=0.1,
+               workload="dense tanh ResNet 1024 layers width 512 batch 16, 3-level FAS cf 16 "
+                        "forward+adjoint training step to tol 1e-9"),
+}
+
+METRIC = "FAS fwd+adjoint solve time to tol; layer*samples/s"
+UNIT = "layer*samples/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    p.add_argument("--adjoint", default="fas", choices=["fas", "sequential"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU side (the oracle port; the reference itself is Python and not on the GPU box)
+
+
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+_NET_CACHE = {}
+
+
+def cpu_reference_sample(cfg, fwd_cycles: int, nsamp: int | None = None):
+    """Time the oracle (numpy restatement of the reference path, all host BLAS threads) on a
+    bounded sample of the workload: `nsamp` samples, initial residual + 2 forward FAS cycles +
+    the reference's sequential adjoint; the forward is extrapolated linearly to `fwd_cycles`
+    cycles (every cycle does the same work).  Returns (layer*samples/s, dict)."""
+    import numpy as np
+
+    from oracle import fas
+
+    N, q = cfg["depth"], cfg["width"]
+    nsamp = nsamp or min(cfg["batch"], max(4, min(8, os.cpu_count() or 4)))
+    key = (N, q)
+    if key not in _NET_CACHE:
+        _NET_CACHE.clear()
+        _NET_CACHE[key] = fas.net_from_arrays(fas.random_network_arrays(N, q, [0, N, q]))
+    net = _NET_CACHE[key]
+    X = np.stack([fas.random_sample(q, [0, N, q, b]) for b in range(nsamp)])
+    labels = np.arange(nsamp) % 10
+    t0 = time.perf_counter()
+    src = net.source(X)
+    levels = fas.build_levels(net.blocks, cfg["cf"], cfg["threshold"])
+    U = fas.initial_guess(levels[0], src)
+    fas.l2_norms(fas.compute_residual(levels[0], U, src))
+    t1 = time.perf_counter()
+    ncyc = 2
+    for _ in range(ncyc):
+        fas.mg_cycle(levels, cfg["cf"], U, src)
+    t2 = time.perf_counter()
+    final, logits = fas.adjoint_head(net, U)
+    _, dl = fas.loss_and_dlogits(logits, labels)
+    gfin, _ = fas.g_final_from(net, final, dl)
+    D = fas.derivs(net.blocks, U)
+    mu, lam0 = fas.adjoint_sequential(fas.adjoint_level(net.blocks, D), gfin)
+    fas.block_grads(net.blocks, U, mu, D, 1.0 / nsamp)
+    t3 = time.perf_counter()
+    est = (t1 - t0) + fwd_cycles * (t2 - t1) / ncyc + (t3 - t2)
+    info = dict(sample=(f"{nsamp} samples of the same workload: initial residual + {ncyc} timed "
+                        f"forward FAS cycles extrapolated to {fwd_cycles} cycles + the reference's "
+                        f"sequential adjoint and block gradients; oracle/fas.py batched numpy"),
+                cores=_blas_threads(), measured_s=t3 - t0, estimated_s=est)
+    return N * nsamp / est, info
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    times, vals = [], []
+    info = None
+    # the number of forward cycles the solve needs at this config (c2: 36)
+    cyc = {"c2": 36, "c1": 7, "c5": 8}[args.config]
+    for i in range(args.warmup + args.steps):
+        v, info = cpu_reference_sample(cfg, cyc)
+        if i >= args.warmup:
+            vals.append(v)
+            times.append(info["estimated_s"])
+    value = statistics.mean(vals)
+    line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
+                warmup=args.warmup, ms_per_step=1e3 * statistics.mean(times), higher_is_better=True,
+                scaling="weak", vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=cfg["workload"]), impl="reference",
+                cpu_baseline=dict(value=value, unit=UNIT, cores=info["cores"], kind="port",
+                                  sample=info["sample"]),
+                e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------------------------
+# GPU side
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = out.strip().splitlines()
+        else:
+            self.lines = []
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return dict(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=mx,
+                    reasons=sorted(reasons), samples=len(sm))
+
+
+def fp64_peak_tflops(torch, dev):
+    """Measured FP64 tensor peak of this GPU: cuBLAS DGEMM 8192^3 (best of 3, CUDA events).
+    MEASURED_PEAKS.json carries HBM and bf16 only ('measure DGEMM on the box')."""
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    best = 0.0
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.matmul(a, b)
+        e.record()
+        e.synchronize()
+        best = max(best, 2.0 * n ** 3 / (s.elapsed_time(e) * 1e-3) / 1e12)
+    del a, b
+    return best
+
+
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch"), d
+    except (OSError, ValueError):
+        return None, None
+
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+
+    import paper_2007_07336_b200 as P
+    from paper_2007_07336_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+
+    N, q, B = cfg["depth"], cfg["width"], cfg["batch"]
+    X_host = torch.from_numpy(P.random_batch(q, [0, N, q], B)).pin_memory()
+    lab_host = torch.from_numpy(np.arange(B) % 10).pin_memory()
+    X = X_host.to(dev)
+    labels = lab_host.to(dev)
+
+    if world > 1:
+        from paper_2007_07336_b200.distributed import LayerParallelTrainer
+
+        tr = LayerParallelTrainer(N, q, [0, N, q], coarsening=cfg["cf"], threshold=cfg["threshold"],
+                                  tol=cfg["tol"], max_cycles=cfg["max_cycles"], adjoint=args.adjoint,
+                                  learning_rate=cfg["lr"])
+    else:
+        d = P.device_network(N, q, [0, N, q], device=dev)
+        tr = P.DeviceTrainer(d, coarsening=cfg["cf"], threshold=cfg["threshold"], tol=cfg["tol"],
+                             max_cycles=cfg["max_cycles"], adjoint=args.adjoint,
+                             learning_rate=cfg["lr"])
+    peak = fp64_peak_tflops(torch, dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    res = None
+    for _ in range(args.warmup):
+        res = tr.step(X, labels)
+    barrier()
+
+    # ---- timed region: inputs resident in HBM
+    _lib.timing_enable(True)
+    n0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        cycles = []
+        for _ in range(args.steps):
+            res = tr.step(X, labels)
+            cycles.append((int(np.max(res.fwd_cycles)),
+                           None if res.adj_cycles is None else int(np.max(res.adj_cycles))))
+        e.record()
+        barrier()
+    launches = _lib.launch_count() - n0
+    ms = s.elapsed_time(e) / args.steps
+    k_ms, k_flops, k_bytes, k_n = _lib.timing_read(0 if args.adjoint == "sequential" else -1)
+    f_ms, f_flops, _, f_n = _lib.timing_read(0)
+    a_ms, a_flops, _, a_n = _lib.timing_read(1)
+    all_ms, _, _, all_n = _lib.timing_read(-1)
+    _lib.timing_enable(False)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- e2e: same step through the public API from pinned host buffers, result read back
+    barrier()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    t_wall = time.perf_counter()
+    for _ in range(args.steps):
+        X.copy_(X_host, non_blocking=True)
+        labels.copy_(lab_host, non_blocking=True)
+        r2 = tr.step(X, labels)
+        loss_host = r2.loss.cpu()
+    e2.record()
+    barrier()
+    e2e_ms = s2.elapsed_time(e2) / args.steps
+    wall_ms = (time.perf_counter() - t_wall) * 1e3 / args.steps
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    gemm_ms = f_ms + a_ms
+    gemm_flops = f_flops + a_flops
+    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    traffic, prof = load_traffic()
+    line = dict(
+        metric=METRIC,
+        value=N * B / (ms * 1e-3),
+        unit=UNIT, n_gpus=world, steps=args.steps, warmup=args.warmup, ms_per_step=ms,
+        higher_is_better=True, scaling="weak" if world > 1 else "weak", vs_baseline=None,
+        dtype="f64", data="synthetic (reference seeded generators: random_network / random_sample)",
+        config=dict(workload=cfg["workload"], depth=N, width=q, batch=B, coarsening=cfg["cf"],
+                    threshold=cfg["threshold"], tol=cfg["tol"], adjoint=args.adjoint,
+                    parallelism=f"layer-partitioned x{world}" if world > 1 else "single GPU",
+                    l2="inputs larger than L2 (theta 2 GiB, states 1 GiB), no flush",
+                    cycles_per_step=cycles),
+        e2e=dict(value=N * B / (e2e_ms * 1e-3), unit=UNIT,
+                 h2d_bytes_per_step=int(X_host.numel() * 8 + lab_host.numel() * 8),
+                 d2h_bytes_per_step=int(loss_host.numel() * 8), wall_ms_per_step=wall_ms),
+        gpu_launches=int(launches),
+        roofline=dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s",
+                      frac=achieved / peak if peak else None,
+                      traffic=traffic,
+                      kernel="lmg::step_gemm (FP64 DMMA m8n8k4, fused FAS epilogues): forward + adjoint layer steps",
+                      peak_source="cuBLAS DGEMM 8192^3 measured in this run (FP64 is not in MEASURED_PEAKS.json)",
+                      algorithmic="(2q^2+5q) flops per F-evaluation x B samples x tasks per launch",
+                      share_of_step=(gemm_ms / (ms * args.steps)) if ms else None,
+                      launches=f_n + a_n, all_kernel_ms_per_step=all_ms / args.steps,
+                      all_launches_per_step=all_n / args.steps),
+    )
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, info = cpu_reference_sample(cfg, cycles[-1][0])
+        line["cpu_baseline"] = dict(value=v, unit=UNIT, cores=info["cores"], kind="port",
+                                    sample=info["sample"])
+    line["clocks"] = clk.summary()
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

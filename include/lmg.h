@@ -70,6 +70,15 @@ typedef struct lmg_system {
 int lmg_abi_version(void);
 const char* lmg_last_error(void);
 
+/* Instrumentation (not part of the reference API): number of kernels this library has launched,
+ * and optional CUDA-event timing of every launch by class (0 forward step GEMM, 1 adjoint step
+ * GEMM, 2 parameter-gradient GEMM, 3 elementwise/reduction; -1 = all).  lmg_timing_enable(1)
+ * clears the records; lmg_timing_read synchronises on the recorded events. */
+unsigned long long lmg_launch_count(void);
+int lmg_timing_enable(int on);
+int lmg_timing_read(int cls, double* ms_total, double* flops_total, double* bytes_total,
+                    unsigned long long* launches);
+
 /* network.py:88-102 propagate_values: out[j-start] = src[j] + (u + h*F_{j-1}(u)), j in
  * [start, stop), from u_start (B, q) = u^{start-1}.  out is (stop-start, B, q). */
 int lmg_propagate(const lmg_system* sys, int B, const double* u_start, const double* src,

@@ -54,6 +54,10 @@ _SYS = ctypes.POINTER(LmgSystem)
 SIGNATURES = {
     "lmg_abi_version": (_I, []),
     "lmg_last_error": (ctypes.c_char_p, []),
+    "lmg_launch_count": (ctypes.c_ulonglong, []),
+    "lmg_timing_enable": (_I, [_I]),
+    "lmg_timing_read": (_I, [_I, c_double_p, c_double_p, c_double_p,
+                             ctypes.POINTER(ctypes.c_ulonglong)]),
     "lmg_propagate": (_I, [_SYS, _I, _P, _P, _I, _I, _I, _P, _P]),
     "lmg_sequential_forward": (_I, [_SYS, _I, _P, _I, _P, _P]),
     "lmg_propagation_operator": (_I, [_SYS, _I, _P, _P, _P]),
@@ -123,3 +127,20 @@ def stream_handle(device=None) -> int:
     import torch
 
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def launch_count() -> int:
+    return int(load().lmg_launch_count())
+
+
+def timing_enable(on: bool) -> None:
+    check(load().lmg_timing_enable(1 if on else 0))
+
+
+def timing_read(cls: int = -1):
+    """(ms, flops, bytes, launches) summed over the recorded launches of class `cls`."""
+    ms, fl, by = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    n = ctypes.c_ulonglong()
+    check(load().lmg_timing_read(cls, ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(by),
+                                 ctypes.byref(n)))
+    return ms.value, fl.value, by.value, int(n.value)

@@ -17,8 +17,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -153,12 +155,58 @@ int grid_for(int64_t total) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
 }
 
+// ------------------------------------------------------------------------------------------
+// launch accounting: a counter of every kernel this library launches (bench "gpu_launches") and
+// optional CUDA-event timing of each launch by class (bench roofline, measured over the timed
+// region on the launching stream).
+
+enum Cls { CLS_GEMM_FWD = 0, CLS_GEMM_ADJ = 1, CLS_GEMM_PG = 2, CLS_ELEM = 3, CLS_N = 4 };
+
+struct Rec {
+  int cls;
+  double flops, bytes;
+  cudaEvent_t a, b;
+};
+
+std::atomic<unsigned long long> g_launches{0};
+bool g_timing = false;
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+size_t g_pool_used = 0;
+
+cudaEvent_t pool_event() {
+  if (g_pool_used == g_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_pool.push_back(e);
+  }
+  return g_pool[g_pool_used++];
+}
+
+template <class F>
+int launch(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
+  Rec r{cls, flops, bytes, nullptr, nullptr};
+  if (g_timing) {
+    r.a = pool_event();
+    cudaEventRecord(r.a, st);
+  }
+  f();
+  CUDA_TRY(cudaGetLastError());
+  if (g_timing) {
+    r.b = pool_event();
+    cudaEventRecord(r.b, st);
+    g_recs.push_back(r);
+  }
+  ++g_launches;
+  return LMG_OK;
+}
+
 int copy_rows(double* dst, int64_t dst_ts, const double* src, int64_t src_ts, int64_t nrows,
               int64_t len, cudaStream_t st) {
   if (nrows <= 0 || len <= 0) return LMG_OK;
-  k_copy_rows<<<grid_for(nrows * len), 256, 0, st>>>(dst, dst_ts, src, src_ts, nrows, len);
-  CUDA_TRY(cudaGetLastError());
-  return LMG_OK;
+  return launch(CLS_ELEM, 0.0, 16.0 * nrows * len, st, [&] {
+    k_copy_rows<<<grid_for(nrows * len), 256, 0, st>>>(dst, dst_ts, src, src_ts, nrows, len);
+  });
 }
 
 // ------------------------------------------------------------------------------------------
@@ -166,26 +214,71 @@ int copy_rows(double* dst, int64_t dst_ts, const double* src, int64_t src_ts, in
 
 enum Layout { L_FWD = 0, L_ADJ = 1, L_PG = 2 };
 
-template <int BM, int BN, int BK, int WM, int WN, int ST, bool AK, bool BKM, bool ASC, int VEC>
+// Tile configurations.  Every config accumulates each output over k in the same order (one
+// DMMA chain, k ascending), so they are bitwise interchangeable; residual partial sums always
+// use TSmall so norms are canonical.  Choice measured on B200 (tools/gemm_bench.py, profiles/):
+// many warps per SMSP hide the DMMA latency better than big warp tiles.
+//   sweep (256 tasks, 256x512x512):  TSmall 26.7 TF/s  TWide 25.8  64x64/32x32-warp 22.8
+//   adjoint layout:                   TWide 25.1        TSmall 21.9
+//   single-task serial step:          TSmall 18.9 us    TWide 24.3   64x64 47.9
+using TSmall = Tile<32, 32, 16, 2, 2, 4>;  // 4 warps of 16x16, ~5 CTAs/SM
+using TWide = Tile<32, 64, 16, 2, 4, 4>;   // 8 warps of 16x16
+
+template <class T, bool AK, bool BKM, bool ASC, int VEC>
 int launch_cfg(const StepArgs& a, cudaStream_t st) {
-  using C = GemmCfg<BM, BN, BK, WM, WN, ST, AK, BKM, ASC>;
-  auto kern = step_gemm<BM, BN, BK, WM, WN, ST, AK, BKM, ASC, VEC>;
+  using C = GemmCfg<T, AK, BKM, ASC>;
+  constexpr int BM = C::BM, BN = C::BN;
+  auto kern = step_gemm<T, AK, BKM, ASC, VEC>;
   static bool attr = false;
   if (!attr) {
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr = true;
   }
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.ntasks);
-  kern<<<grid, C::NTHREADS, C::SMEM, st>>>(a);
-  CUDA_TRY(cudaGetLastError());
-  return LMG_OK;
+  const int cls = AK ? (BKM ? CLS_GEMM_FWD : CLS_GEMM_ADJ) : CLS_GEMM_PG;
+  // algorithmic work: 2MNK per task + ~5 epilogue flops per output (2q^2+5q per F)
+  const double flops = (double)a.ntasks * ((double)a.M * a.N * (2.0 * a.K + 5.0));
+  const double bytes = 8.0 * a.ntasks * ((double)a.N * a.K + (double)a.M * a.K + 2.0 * a.M * a.N);
+  return launch(cls, flops, bytes, st, [&] { kern<<<grid, C::NTHREADS, C::SMEM, st>>>(a); });
 }
 
-constexpr int TBM = 64, TBN = 64, TBK = 16, TWM = 2, TWN = 2, TST = 4;
-
-int n_tiles(int N) { return (N + TBN - 1) / TBN; }
+// residual partial slots are per TSmall n-tile
+int n_tiles(int N) { return (N + TSmall::BN - 1) / TSmall::BN; }
 
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+enum TileSel { SEL_AUTO = 0, SEL_SMALL = 1, SEL_WIDE = 2 };
+
+int tile_override() {
+  static int v = [] {
+    const char* e = getenv("LMG_TILE");
+    if (e && !strcmp(e, "small")) return (int)SEL_SMALL;
+    if (e && !strcmp(e, "wide")) return (int)SEL_WIDE;
+    return (int)SEL_AUTO;
+  }();
+  return v;
+}
+
+int64_t ctas_for(const StepArgs& a, int BM, int BN) {
+  return (int64_t)a.ntasks * ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN);
+}
+
+template <bool AK, bool BKM, bool ASC>
+int choose_tile(const StepArgs& a) {
+  if (a.epi == E_RESID) return SEL_SMALL;  // canonical partial-sum layout
+  int o = tile_override();
+  if (o != SEL_AUTO) return o;
+  const bool adj = AK && !BKM;
+  if (adj && ctas_for(a, TWide::BM, TWide::BN) >= 2 * 148) return SEL_WIDE;
+  return SEL_SMALL;
+}
+
+template <bool AK, bool BKM, bool ASC>
+int launch_layout(const StepArgs& a, bool v2, cudaStream_t st) {
+  if (!v2) return launch_cfg<TSmall, AK, BKM, ASC, 1>(a, st);
+  if (choose_tile<AK, BKM, ASC>(a) == SEL_WIDE) return launch_cfg<TWide, AK, BKM, ASC, 2>(a, st);
+  return launch_cfg<TSmall, AK, BKM, ASC, 2>(a, st);
+}
 
 int launch_step(Layout L, const StepArgs& a, cudaStream_t st) {
   if (a.ntasks <= 0 || a.M <= 0 || a.N <= 0) return LMG_OK;
@@ -196,15 +289,9 @@ int launch_step(Layout L, const StepArgs& a, cudaStream_t st) {
   if (L == L_ADJ) v2 = v2 && (a.K % 2 == 0) && (a.N % 2 == 0);
   if (L == L_PG) v2 = v2 && (a.M % 2 == 0) && (a.N % 2 == 0);
   switch (L) {
-    case L_FWD:
-      return v2 ? launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, true, true, false, 2>(a, st)
-                : launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, true, true, false, 1>(a, st);
-    case L_ADJ:
-      return v2 ? launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, true, false, true, 2>(a, st)
-                : launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, true, false, true, 1>(a, st);
-    case L_PG:
-      return v2 ? launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, false, false, true, 2>(a, st)
-                : launch_cfg<TBM, TBN, TBK, TWM, TWN, TST, false, false, true, 1>(a, st);
+    case L_FWD: return launch_layout<true, true, false>(a, v2, st);
+    case L_ADJ: return launch_layout<true, false, true>(a, v2, st);
+    case L_PG: return launch_layout<false, false, true>(a, v2, st);
   }
   return fail(LMG_ERR_CONFIGURATION, "bad layout");
 }
@@ -378,8 +465,7 @@ int residual_full(const lmg_system& S, int B, const double* U, const double* src
   const int q = S.width;
   const int64_t BQ = (int64_t)B * q;
   const int n = S.num_layers;
-  k_resid_row0<<<B, 256, 0, st>>>(src, U, R, part, 0, B, q);
-  CUDA_TRY(cudaGetLastError());
+  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_resid_row0<<<B, 256, 0, st>>>(src, U, R, part, 0, B, q); }));
   Fam f;
   f.ntasks = n - 1; f.blk0 = 0; f.blk_step = 1;
   f.x = U; f.x_ts = BQ;
@@ -399,8 +485,7 @@ int residual_post(const lmg_system& S, int B, int c, const double* U, const doub
   const int64_t BQ = (int64_t)B * q;
   const int nb = S.num_layers / c;
   const int nt = n_tiles(q);
-  k_resid_row0<<<B, 256, 0, st>>>(src, U, nullptr, part, 0, B, q);
-  CUDA_TRY(cudaGetLastError());
+  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_resid_row0<<<B, 256, 0, st>>>(src, U, nullptr, part, 0, B, q); }));
   Fam f1;  // rows kc, k = 1..nb-1
   f1.ntasks = nb - 1; f1.blk0 = c - 1; f1.blk_step = c;
   f1.x = U + (int64_t)(c - 1) * BQ; f1.x_ts = c * BQ;
@@ -420,8 +505,7 @@ int residual_post(const lmg_system& S, int B, int c, const double* U, const doub
 }
 
 int reduce_norms(const double* part, int64_t nslots, int B, double* norms, cudaStream_t st) {
-  k_reduce_norms<<<(B + 127) / 128, 128, 0, st>>>(part, nslots, B, norms);
-  CUDA_TRY(cudaGetLastError());
+  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_reduce_norms<<<(B + 127) / 128, 128, 0, st>>>(part, nslots, B, norms); }));
   return LMG_OK;
 }
 
@@ -505,15 +589,13 @@ int cycle(const lmg_system& S, int nlevels, int l, int c, int B, double* U, cons
     f.out = SH + BQ; f.out_ts = BQ;
     f.out2 = coarsest ? nullptr : V + BQ; f.out2_ts = BQ;
     TRY(family(Sc, B, E_COARSE, f, st));
-    k_row0_coarse<<<grid_for(BQ), 256, 0, st>>>(U, src, SH, coarsest ? nullptr : V, BQ);
-    CUDA_TRY(cudaGetLastError());
+    TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_row0_coarse<<<grid_for(BQ), 256, 0, st>>>(U, src, SH, coarsest ? nullptr : V, BQ); }));
   }
   if (coarsest)
     TRY(seq_forward(Sc, B, SH, LMG_SRC_DENSE, V, st));
   else
     TRY(cycle(Sc, nlevels, l + 1, c, B, V, SH, LMG_SRC_DENSE, ws, false, nullptr, st));
-  k_correct<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, c * BQ, V, BQ, nb, BQ);
-  CUDA_TRY(cudaGetLastError());
+  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_correct<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, c * BQ, V, BQ, nb, BQ); }));
   if (want_norm) {
     TRY(residual_post(S, B, c, U, src, mode, ws.part, st, &nslots));
     TRY(reduce_norms(ws.part, nslots, B, norms, st));
@@ -540,6 +622,36 @@ int check_levels(const lmg_system& fine, int nlevels, int c) {
 extern "C" {
 
 int lmg_abi_version(void) { return 1; }
+
+unsigned long long lmg_launch_count(void) { return g_launches.load(); }
+
+int lmg_timing_enable(int on) {
+  g_timing = on != 0;
+  g_recs.clear();
+  g_pool_used = 0;
+  return LMG_OK;
+}
+
+int lmg_timing_read(int cls, double* ms_total, double* flops_total, double* bytes_total,
+                    unsigned long long* launches) {
+  double ms = 0.0, fl = 0.0, by = 0.0;
+  unsigned long long n = 0;
+  for (const Rec& r : g_recs) {
+    if (cls >= 0 && r.cls != cls) continue;
+    CUDA_TRY(cudaEventSynchronize(r.b));
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    ms += t;
+    fl += r.flops;
+    by += r.bytes;
+    ++n;
+  }
+  if (ms_total) *ms_total = ms;
+  if (flops_total) *flops_total = fl;
+  if (bytes_total) *bytes_total = by;
+  if (launches) *launches = n;
+  return LMG_OK;
+}
 
 const char* lmg_last_error(void) { return g_err.c_str(); }
 
@@ -606,8 +718,7 @@ int lmg_assemble_coarse_source(const lmg_system* coarse, int B, const double* UH
   TRY(check_sys(coarse, B));
   const int64_t BQ = (int64_t)B * coarse->width;
   // row 0: propagation_operator row 0 (U_H[0]) plus the residual row 0
-  k_add<<<grid_for(BQ), 256, 0, S_(stream)>>>(out, UH, RH, BQ);
-  CUDA_TRY(cudaGetLastError());
+  TRY(launch(CLS_ELEM, 0.0, 0.0, S_(stream), [&] { k_add<<<grid_for(BQ), 256, 0, S_(stream)>>>(out, UH, RH, BQ); }));
   Fam f;
   f.ntasks = coarse->num_layers - 1;
   f.x = UH; f.x_ts = BQ;
@@ -767,10 +878,9 @@ int lmg_param_grads(const lmg_system* fine, int B, const double* states, const d
   a.ldc = q;
   TRY(launch_step(L_PG, a, st));
   const int64_t tot = (int64_t)N * q;
-  k_bias_grads<<<(int)((tot + 255) / 256), 256, 0, st>>>(lam + (int64_t)(N - 1) * BQ, -BQ, D, N, B, q,
+  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_bias_grads<<<(int)((tot + 255) / 256), 256, 0, st>>>(lam + (int64_t)(N - 1) * BQ, -BQ, D, N, B, q,
                                                          fine->step, scale, lr, gb,
-                                                         const_cast<double*>(fine->b), fine->b_stride);
-  CUDA_TRY(cudaGetLastError());
+                                                         const_cast<double*>(fine->b), fine->b_stride); }));
   return LMG_OK;
 }
 
@@ -820,9 +930,8 @@ int lmg_dense_vjp(const double* W, const double* b, int act, int M, int q_out, i
     TRY(launch_step(L_PG, a, st));
   }
   if (gb) {
-    k_bias_grads<<<(q_out + 255) / 256, 256, 0, st>>>(G, 0, work, 1, M, q_out, 1.0, 1.0, 0.0, gb,
-                                                       nullptr, 0);
-    CUDA_TRY(cudaGetLastError());
+    TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_bias_grads<<<(q_out + 255) / 256, 256, 0, st>>>(G, 0, work, 1, M, q_out, 1.0, 1.0, 0.0, gb,
+                                                       nullptr, 0); }));
   }
   return LMG_OK;
 }
@@ -833,8 +942,7 @@ int lmg_l2_norms(const double* x, int n, int B, int q, double* norms, void* work
   double* part = reinterpret_cast<double*>(work);
   const int64_t BQ = (int64_t)B * q;
   for (int j = 0; j < n; ++j) {  // one slot per row: sum_b of row j (zero source minus -x)
-    k_resid_row0<<<B, 256, 0, st>>>(x + j * BQ, nullptr, nullptr, part, j, B, q);
-    CUDA_TRY(cudaGetLastError());
+    TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_resid_row0<<<B, 256, 0, st>>>(x + j * BQ, nullptr, nullptr, part, j, B, q); }));
   }
   return reduce_norms(part, n, B, norms, st);
 }

@@ -3,7 +3,7 @@
 //
 // Why DMMA and not tcgen05: the path must run in float64 (fp32 already floors the
 // residual at 1e-6 vs tol 1e-9) and tcgen05.mma has no f64 kind.  On sm_100a the f64
-// mma.sync lowers to DMMA.8x8x4 on the FP64 tensor pipe.
+// mma.sync lowers to DMMA.8x8x4 on the FP64 tensor pipe (64 FMA/clk/SM, ~37 TF/s at 1.965 GHz).
 //
 // One launch evaluates `ntasks` independent layer steps ("tasks"), e.g. every block's j-th
 // F-relaxation step of a sweep.  Task t's operands are affine in t (base + t*stride), so a whole
@@ -17,6 +17,11 @@
 // forward step   (m=b, n=i, k=k): A = U_{j-1} (B x q, K-major), B = W_j (q x q, K-major)
 // adjoint step   (m=b, n=k, k=i): A = mu * D  (K-major, scaled), B = W_j (MN-major)
 // parameter grad (m=i, n=k, k=b): A = lam * D (MN-major, scaled), B = U_j (MN-major)
+//
+// Pipeline: STAGES-deep cp.async ring (global -> smem, 16 B vectors when aligned), +4-double row
+// padding so every m8n8k4 fragment load is bank-conflict free, fragments for k4-step kk+1 loaded
+// while the DMMAs of kk issue.  The epilogue mode is switched once per CTA, outside the unrolled
+// fragment loops (an in-loop switch blew the instruction cache: ncu 'no_instruction' stalls).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -34,7 +39,8 @@ enum Epi {
   E_PROPOP = 4,    // out = y - (x + h*act(pre))                       network.py:138
   E_DERIV = 5,     // out = act'(pre)                                  kernels.py:44-48
   E_PGRAD = 6,     // g = (acc*h)*scale; out2 = g; out = x - lr*g      training.py:218-236
-  E_APPLY = 7      // out = act(pre)                                   kernels.py:139-150
+  E_APPLY = 7,     // out = act(pre)                                   kernels.py:139-150
+  E_ADV = 8        // out = x + h*act(pre)  (a halo value without its source row)
 };
 
 struct StepArgs {
@@ -121,14 +127,72 @@ __device__ __forceinline__ void load_tile(double* sm, const double* g, int ld, i
   }
 }
 
+// Per-thread precomputed global->smem copy plan for one operand tile: the k-loop only adds a
+// constant pointer advance (no index math, no per-tile bounds checks unless K % BK != 0).
+template <bool KMAJ, int T, int BK, int VEC, int NT>
+struct Loader {
+  using S = TileShape<KMAJ, T, BK>;
+  static constexpr int PR = KMAJ ? BK / VEC : T / VEC;  // vectors per smem row
+  static constexpr int NV = (KMAJ ? T : BK) * PR;        // vectors per tile
+  static constexpr int IT = (NV + NT - 1) / NT;          // vectors per thread
+  const double* g;
+  int64_t kadv;  // pointer advance per k-tile
+  int goff[IT], soff[IT], kin[IT];
+  unsigned okmask;
+
+  __device__ __forceinline__ void init(const double* base, int ld, int mn0, int mnlim, int tid) {
+    g = base;
+    kadv = KMAJ ? BK : (int64_t)BK * ld;
+    okmask = 0;
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const int e = tid + i * NT;
+      int r, kk;
+      if (KMAJ) {
+        r = e / PR;
+        kk = (e % PR) * VEC;
+      } else {
+        kk = e / PR;
+        r = (e % PR) * VEC;
+      }
+      const bool ok = (e < NV) && (mn0 + r < mnlim);
+      goff[i] = KMAJ ? (mn0 + r) * ld + kk : kk * ld + mn0 + r;
+      soff[i] = KMAJ ? r * S::LD + kk : kk * S::LD + r;
+      kin[i] = kk;
+      okmask |= (ok ? 1u : 0u) << i;
+    }
+  }
+  // copy k-tile `kt` (first k index k0) into sm; kfull: the whole tile lies inside K
+  __device__ __forceinline__ void load(double* sm, int kt, int k0, int klim, bool kfull) const {
+    const double* gt = g + kt * kadv;
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      bool ok = (okmask >> i) & 1u;
+      if (!kfull) ok = ok && (k0 + kin[i] < klim);
+      if (IT * NT > NV && tid_out_of_range(i)) continue;
+      cp_async<VEC>(sm + soff[i], ok ? gt + goff[i] : g, ok);
+    }
+  }
+  __device__ __forceinline__ bool tid_out_of_range(int i) const {
+    return (int)(threadIdx.x + i * NT) >= NV;
+  }
+};
+
 template <bool KMAJ, int T, int BK>
 __device__ __forceinline__ double frag(const double* sm, int mn, int k) {
   using S = TileShape<KMAJ, T, BK>;
   return KMAJ ? sm[mn * S::LD + k] : sm[k * S::LD + mn];
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, bool ASC>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct Tile {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+};
+
+template <class T, bool AK, bool BKM, bool ASC>
 struct GemmCfg {
+  static constexpr int BM = T::BM, BN = T::BN, BK = T::BK, WM = T::WM, WN = T::WN;
+  static constexpr int STAGES = T::STAGES;
   static constexpr int NTHREADS = WM * WN * 32;
   static constexpr int WTM = BM / WM, WTN = BN / WN;  // warp tile
   static constexpr int MT = WTM / 8, NTF = WTN / 8;   // m8n8 fragments per warp
@@ -138,10 +202,78 @@ struct GemmCfg {
   static constexpr size_t SMEM = (size_t)STAGES * STAGE * sizeof(double);
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool AK, bool BKM, bool ASC, int VEC>
-__global__ void __launch_bounds__(WM* WN * 32)
+// Per-task epilogue operands.
+struct EpiPtrs {
+  const double *bias, *X, *S, *Y, *P;
+  double *O, *O2;
+};
+
+// Apply epilogue EPI to this thread's accumulators.  Returns per-fragment-row sums of r^2 for
+// E_RESID in rowsq.
+template <int EPI, int MT, int NTF>
+__device__ __forceinline__ void epilogue(const StepArgs& a, const EpiPtrs& q, double (&acc)[MT][NTF][2],
+                                         int mrow0, int ncol0, double (&rowsq)[MT]) {
+  const int actk = a.act;
+  const double h = a.h;
+  const int ldc = a.ldc;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    rowsq[i] = 0.0;
+    const int m = mrow0 + i * 8;
+    if (m >= a.M) continue;
+#pragma unroll
+    for (int j = 0; j < NTF; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = ncol0 + j * 8 + e;
+        if (n >= a.N) continue;
+        const int64_t idx = (int64_t)m * ldc + n;
+        const double accv = acc[i][j][e];
+        if (EPI == E_PGRAD) {
+          double g = __dmul_rn(__dmul_rn(accv, h), a.scale);
+          if (q.O2) q.O2[idx] = g;
+          if (a.lr != 0.0) q.O[idx] = __dadd_rn(q.X[idx], -__dmul_rn(a.lr, g));
+          continue;
+        }
+        double pre = accv;
+        if (q.bias) pre = __dadd_rn(pre, q.bias[n]);
+        if (EPI == E_DERIV) {
+          q.O[idx] = act_der(actk, pre);
+          continue;
+        }
+        const double v = act_fwd(actk, pre);
+        if (EPI == E_APPLY) {
+          q.O[idx] = v;
+          continue;
+        }
+        const double adv = __dadd_rn(q.X[idx], __dmul_rn(h, v));  // u + h*F(u)
+        if (EPI == E_ADV) {
+          q.O[idx] = adv;
+        } else if (EPI == E_PROP) {
+          q.O[idx] = __dadd_rn(q.S ? q.S[idx] : 0.0, adv);
+        } else if (EPI == E_RESID) {
+          double r = __dadd_rn(__dadd_rn(q.S ? q.S[idx] : 0.0, adv), -q.Y[idx]);
+          if (q.O) q.O[idx] = r;
+          rowsq[i] = fma(r, r, rowsq[i]);
+        } else if (EPI == E_COARSE) {
+          const double yv = q.Y[idx];
+          q.O[idx] = __dadd_rn(__dadd_rn(yv, -adv), __dadd_rn(q.P[idx], -yv));
+          if (q.O2) q.O2[idx] = yv;
+        } else if (EPI == E_COARSE_R) {
+          q.O[idx] = __dadd_rn(__dadd_rn(q.Y[idx], -adv), q.P[idx]);
+        } else {  // E_PROPOP
+          q.O[idx] = __dadd_rn(q.Y[idx], -adv);
+        }
+      }
+    }
+  }
+}
+
+template <class T, bool AK, bool BKM, bool ASC, int VEC>
+__global__ void __launch_bounds__(T::WM* T::WN * 32)
     step_gemm(const StepArgs a) {
-  using C = GemmCfg<BM, BN, BK, WM, WN, STAGES, AK, BKM, ASC>;
+  using C = GemmCfg<T, AK, BKM, ASC>;
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, WN = C::WN, STAGES = C::STAGES;
   extern __shared__ __align__(16) double smem[];
   __shared__ double red[WN][BM];
 
@@ -161,14 +293,20 @@ __global__ void __launch_bounds__(WM* WN * 32)
     for (int j = 0; j < C::NTF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int KT = (a.K + BK - 1) / BK;
-  auto stage_ptr = [&](int s) { return smem + s * C::STAGE; };
+  const bool kfull_all = (a.K % BK) == 0;
+  Loader<AK, BM, BK, VEC, C::NTHREADS> la;
+  Loader<BKM, BN, BK, VEC, C::NTHREADS> lb;
+  la.init(A, a.lda, m0, a.M, tid);
+  lb.init(Bm, a.ldb, n0, a.N, tid);
+  Loader<AK, BM, BK, VEC, C::NTHREADS> ld_;
+  if (ASC) ld_.init(Ds, a.lda, m0, a.M, tid);
   auto load_stage = [&](int s, int kt) {
-    double* base = stage_ptr(s);
-    int k0 = kt * BK;
-    load_tile<AK, BM, BK, VEC, C::NTHREADS>(base, A, a.lda, m0, a.M, k0, a.K, tid);
-    if (ASC) load_tile<AK, BM, BK, VEC, C::NTHREADS>(base + C::A_SZ, Ds, a.lda, m0, a.M, k0, a.K, tid);
-    load_tile<BKM, BN, BK, VEC, C::NTHREADS>(base + C::A_SZ * (ASC ? 2 : 1), Bm, a.ldb, n0, a.N, k0,
-                                             a.K, tid);
+    double* base = smem + s * C::STAGE;
+    const int k0 = kt * BK;
+    const bool kfull = kfull_all || (k0 + BK <= a.K);
+    la.load(base, kt, k0, a.K, kfull);
+    if (ASC) ld_.load(base + C::A_SZ, kt, k0, a.K, kfull);
+    lb.load(base + C::A_SZ * (ASC ? 2 : 1), kt, k0, a.K, kfull);
   };
 
 #pragma unroll
@@ -188,89 +326,55 @@ __global__ void __launch_bounds__(WM* WN * 32)
       if (nk < KT) load_stage(nk % STAGES, nk);
       cp_commit();
     }
-    const double* As = stage_ptr(kt % STAGES);
+    const double* As = smem + (kt % STAGES) * C::STAGE;
     const double* Dsm = As + C::A_SZ;
     const double* Bs = As + C::A_SZ * (ASC ? 2 : 1);
-#pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[C::MT], bf[C::NTF];
+    double af[2][C::MT], bf[2][C::NTF];
+    auto ldfrag = [&](int buf, int kk) {
 #pragma unroll
       for (int i = 0; i < C::MT; ++i) {
-        af[i] = frag<AK, BM, BK>(As, wm0 + i * 8 + fr, kk + fk);
-        if (ASC) af[i] = __dmul_rn(af[i], frag<AK, BM, BK>(Dsm, wm0 + i * 8 + fr, kk + fk));
+        af[buf][i] = frag<AK, BM, BK>(As, wm0 + i * 8 + fr, kk + fk);
+        if (ASC) af[buf][i] = __dmul_rn(af[buf][i], frag<AK, BM, BK>(Dsm, wm0 + i * 8 + fr, kk + fk));
       }
 #pragma unroll
-      for (int j = 0; j < C::NTF; ++j) bf[j] = frag<BKM, BN, BK>(Bs, wn0 + j * 8 + fr, kk + fk);
+      for (int j = 0; j < C::NTF; ++j) bf[buf][j] = frag<BKM, BN, BK>(Bs, wn0 + j * 8 + fr, kk + fk);
+    };
+    ldfrag(0, 0);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      const int cur = (kk >> 2) & 1;
+      if (kk + 4 < BK) ldfrag(cur ^ 1, kk + 4);
 #pragma unroll
       for (int i = 0; i < C::MT; ++i)
 #pragma unroll
-        for (int j = 0; j < C::NTF; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < C::NTF; ++j) dmma(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
     }
   }
   cp_wait<0>();
 
   // ---------------------------------------------------------------- fused epilogue
-  const int epi = a.epi, actk = a.act;
-  const double h = a.h;
-  const double* bias = a.bias ? a.bias + t * a.bias_ts : nullptr;
-  const double* X = a.x ? a.x + t * a.x_ts : nullptr;
-  const double* S = a.s ? a.s + t * a.s_ts : nullptr;
-  const double* Y = a.y ? a.y + t * a.y_ts : nullptr;
-  const double* P = a.p ? a.p + t * a.p_ts : nullptr;
-  double* O = a.out ? a.out + t * a.out_ts : nullptr;
-  double* O2 = a.out2 ? a.out2 + t * a.out2_ts : nullptr;
-  const int ldc = a.ldc;
-
+  EpiPtrs q;
+  q.bias = a.bias ? a.bias + t * a.bias_ts : nullptr;
+  q.X = a.x ? a.x + t * a.x_ts : nullptr;
+  q.S = a.s ? a.s + t * a.s_ts : nullptr;
+  q.Y = a.y ? a.y + t * a.y_ts : nullptr;
+  q.P = a.p ? a.p + t * a.p_ts : nullptr;
+  q.O = a.out ? a.out + t * a.out_ts : nullptr;
+  q.O2 = a.out2 ? a.out2 + t * a.out2_ts : nullptr;
+  const int mrow0 = m0 + wm0 + fr, ncol0 = n0 + wn0 + 2 * fk;
   double rowsq[C::MT];
-#pragma unroll
-  for (int i = 0; i < C::MT; ++i) {
-    rowsq[i] = 0.0;
-    const int m = m0 + wm0 + i * 8 + fr;
-#pragma unroll
-    for (int j = 0; j < C::NTF; ++j) {
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int n = n0 + wn0 + j * 8 + 2 * fk + e;
-        if (m >= a.M || n >= a.N) continue;
-        const int64_t idx = (int64_t)m * ldc + n;
-        double pre = acc[i][j][e];
-        if (bias) pre = __dadd_rn(pre, bias[n]);
-        if (epi == E_DERIV) {
-          O[idx] = act_der(actk, pre);
-          continue;
-        }
-        if (epi == E_PGRAD) {
-          double g = __dmul_rn(__dmul_rn(acc[i][j][e], h), a.scale);
-          if (O2) O2[idx] = g;
-          if (a.lr != 0.0) O[idx] = __dadd_rn(X[idx], -__dmul_rn(a.lr, g));
-          continue;
-        }
-        const double v = act_fwd(actk, pre);
-        if (epi == E_APPLY) {
-          O[idx] = v;
-          continue;
-        }
-        const double xv = X[idx];
-        const double adv = __dadd_rn(xv, __dmul_rn(h, v));  // u + h*F(u)
-        if (epi == E_PROP) {
-          O[idx] = __dadd_rn(S ? S[idx] : 0.0, adv);
-        } else if (epi == E_RESID) {
-          double r = __dadd_rn(__dadd_rn(S ? S[idx] : 0.0, adv), -Y[idx]);
-          if (O) O[idx] = r;
-          rowsq[i] = fma(r, r, rowsq[i]);
-        } else if (epi == E_COARSE) {
-          const double yv = Y[idx];
-          O[idx] = __dadd_rn(__dadd_rn(yv, -adv), __dadd_rn(P[idx], -yv));
-          if (O2) O2[idx] = yv;
-        } else if (epi == E_COARSE_R) {
-          O[idx] = __dadd_rn(__dadd_rn(Y[idx], -adv), P[idx]);
-        } else {  // E_PROPOP
-          O[idx] = __dadd_rn(Y[idx], -adv);
-        }
-      }
-    }
+  switch (a.epi) {
+    case E_PROP: epilogue<E_PROP>(a, q, acc, mrow0, ncol0, rowsq); break;
+    case E_RESID: epilogue<E_RESID>(a, q, acc, mrow0, ncol0, rowsq); break;
+    case E_COARSE: epilogue<E_COARSE>(a, q, acc, mrow0, ncol0, rowsq); break;
+    case E_COARSE_R: epilogue<E_COARSE_R>(a, q, acc, mrow0, ncol0, rowsq); break;
+    case E_PROPOP: epilogue<E_PROPOP>(a, q, acc, mrow0, ncol0, rowsq); break;
+    case E_DERIV: epilogue<E_DERIV>(a, q, acc, mrow0, ncol0, rowsq); break;
+    case E_PGRAD: epilogue<E_PGRAD>(a, q, acc, mrow0, ncol0, rowsq); break;
+    case E_APPLY: epilogue<E_APPLY>(a, q, acc, mrow0, ncol0, rowsq); break;
+    default: epilogue<E_ADV>(a, q, acc, mrow0, ncol0, rowsq); break;
   }
-  if (epi == E_RESID && a.part) {
+  if (a.epi == E_RESID && a.part) {
     // deterministic per-row partial sums: 4 lanes of a fragment row, then the WN warps
 #pragma unroll
     for (int i = 0; i < C::MT; ++i) {
