@@ -147,6 +147,39 @@ int lmg_param_grads(const lmg_system* fine, int B, const double* states, const d
                     const double* D, double scale, double lr, double* gW, double* gb,
                     void* stream);
 
+/* ---- layer-partitioned level operations -------------------------------------------
+ * A rank owns L = nb*c consecutive states of a level (nb whole blocks of the reference's
+ * BlockPartition, parallel.py:61-79).  U has L rows plus, when has_next, one outgoing halo row
+ * U[L]; a dense src has the matching rows (+ a zero row L); P has nb+1 rows (P[0] incoming,
+ * P[nb] outgoing).  Halo values travel WITHOUT their source row ("adv" = u + h F(u)); the receiver
+ * finishes them with lmg_halo_finish.  Per cycle and cross edge: U[L] after fcf_a (the
+ * reference's one BoundaryMessage per edge per C-sweep, parallel.py:183-216), then P[nb] and
+ * adv_out after fcf_b.  Single GPU == is_first = 1, has_next = 0.  States are bitwise identical
+ * for every partition; norms too, since partials are per block and summed in global block order.
+ */
+int lmg_local_fcf_a(const lmg_system* sys, int B, int c, double* U, const double* src,
+                    int src_mode, int is_first, int has_next, void* stream);
+int lmg_local_fcf_b(const lmg_system* sys, int B, int c, double* U, const double* src,
+                    int src_mode, double* P, int has_next, double* adv_out, void* stream);
+int lmg_halo_finish(const double* s0, const double* adv_in, double* out, int64_t len, void* stream);
+int lmg_local_coarse_source(const lmg_system* sys, int B, int c, const double* U,
+                            const double* src, int src_mode, const double* P,
+                            const double* adv_in, int is_first, double* SH, double* V,
+                            void* stream);
+int lmg_local_correct(int n_blocks, int B, int q, int c, double* U, const double* V, void* stream);
+size_t lmg_local_workspace(int L, int B, int q);
+int lmg_local_residual_post(const lmg_system* sys, int B, int c, const double* U,
+                            const double* src, int src_mode, const double* P, int is_first,
+                            double* block_part, void* work, void* stream);
+int lmg_local_residual_full_a(const lmg_system* sys, int B, const double* U, const double* src,
+                              int src_mode, int has_next, double* adv_out, void* work,
+                              void* stream);
+int lmg_local_residual_full_b(const lmg_system* sys, int B, int c, const double* U,
+                              const double* src, int src_mode, const double* adv_in, int is_first,
+                              double* block_part, void* work, void* stream);
+int lmg_norms_from_blocks(const double* block_part, int nblocks, int B, double* norms,
+                          void* stream);
+
 /* kernels.py:139-150 apply_transform (dense) for a batch: Y (M, q_out) = act(X W^T + b),
  * X (M, q_in), W (q_out, q_in) row-major, b (q_out) or NULL. */
 int lmg_dense_apply(const double* W, const double* b, int act, int M, int q_out, int q_in,

@@ -150,6 +150,85 @@ __global__ void k_bias_grads(const double* __restrict__ lam_top, int64_t lam_ts,
   }
 }
 
+// out = (s0 ? s0 : 0.0) + adv: finish a halo value received from the previous rank with this
+// rank's own source row (network.py:100 `source[j] + (u + h*fv)`).
+__global__ void k_halo_finish(const double* __restrict__ s0, const double* __restrict__ adv,
+                              double* __restrict__ out, int64_t len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __dadd_rn(s0 ? s0[i] : 0.0, adv[i]);
+}
+
+// first coarse-source row of a non-first rank: S_H[0] = (U[0] - adv_in) + (P[0] - U[0]), where
+// adv_in = U_prev + H*F(U_prev) came from the previous rank (multigrid.py:142, network.py:138)
+__global__ void k_row0_coarse_halo(const double* __restrict__ U0, const double* __restrict__ adv,
+                                   const double* __restrict__ P0, double* __restrict__ SH0,
+                                   double* __restrict__ V0, int64_t len) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double u = U0[i];
+    SH0[i] = __dadd_rn(__dadd_rn(u, -adv[i]), __dadd_rn(P0[i], -u));
+    if (V0) V0[i] = u;
+  }
+}
+
+// C-row residual partials after the correction: block k, sample b:
+//   r = (k == 0 && is_first) ? f[0] - U[0] : P[k] - U[kc]        (multigrid.py:124-127)
+// one CTA per (k, b), fixed-order tree reduction -> cpart[k*B + b]
+__global__ void k_cpart(const double* __restrict__ U, const double* __restrict__ P,
+                        const double* __restrict__ S0, int is_first, int c, int B, int q,
+                        double* __restrict__ cpart) {
+  __shared__ double sh[256];
+  const int k = blockIdx.y, b = blockIdx.x;
+  const int64_t BQ = (int64_t)B * q;
+  const double* u = U + (int64_t)k * c * BQ + (int64_t)b * q;
+  const double* p = (k == 0 && is_first) ? (S0 ? S0 + (int64_t)b * q : nullptr)
+                                         : P + (int64_t)k * BQ + (int64_t)b * q;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    double r = __dadd_rn(p ? p[i] : 0.0, -u[i]);
+    acc = fma(r, r, acc);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cpart[(int64_t)k * B + b] = sh[0];
+}
+
+// block partials after the correction: block_part[k][b] = cpart[k][b] + sum_t fpart[k][t][b]
+__global__ void k_combine_post(const double* __restrict__ cpart, const double* __restrict__ fpart,
+                               int nb, int nt, int B, double* __restrict__ block_part) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nb * B) return;
+  int k = (int)(e / B), b = (int)(e - (int64_t)k * B);
+  double s = cpart[e];
+  for (int t = 0; t < nt; ++t) s += fpart[((int64_t)k * nt + t) * B + b];
+  block_part[e] = s;
+}
+
+// block partials of a full residual: block k = sum over its c rows (row order), each row the sum
+// of its tile partials; row 0 of the rank comes from r0part
+__global__ void k_combine_full(const double* __restrict__ rpart, const double* __restrict__ r0part,
+                               int nb, int c, int nt, int B, double* __restrict__ block_part) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nb * B) return;
+  int k = (int)(e / B), b = (int)(e - (int64_t)k * B);
+  double s = 0.0;
+  for (int j = k * c; j < (k + 1) * c; ++j) {
+    if (j == 0) {
+      s += r0part[b];
+      continue;
+    }
+    double rs = 0.0;
+    for (int t = 0; t < nt; ++t) rs += rpart[((int64_t)j * nt + t) * B + b];
+    s += rs;
+  }
+  block_part[e] = s;
+}
+
 int grid_for(int64_t total) {
   int64_t g = (total + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
@@ -434,29 +513,197 @@ int c_relax(const lmg_system& S, int B, int c, double* U, const double* src, int
   return copy_rows(U, 0, src, 0, 1, BQ, st);
 }
 
-// Fused FCF (bitwise identical to F, C, F): launch s = 0..c-2 runs block k-1's first F step s+1
-// for every k >= 1 (writing the block's F rows, which the reference also does), s = c-1 the C
-// step, s = c..2c-2 the second F sweep.  Each C row's old value is consumed at s = 0, before the
-// C step overwrites it at s = c-1, and block nb-1's first F sweep (dead in the reference) is
-// skipped.  If P != NULL a final step writes P[k+1] = propagate(U[(k+1)c-1]) for k < nb-1: the
-// propagated value of every interior C row, i.e. the C-row residual R[kc] = P[k] - U[kc].
-int fcf(const lmg_system& S, int B, int c, double* U, const double* src, int mode, double* P,
-        cudaStream_t st) {
+// ---- partition-aware ("local") level operations -----------------------------------------
+// A rank holds L = nb*c consecutive states of a level: U has L rows (+1 outgoing halo slot when
+// has_next), src is the head (row 0 only) or dense rows (+1 zero row when has_next), P has nb+1
+// rows (P[0] incoming from the previous rank, P[nb] outgoing).  The single-GPU solve is the
+// special case is_first = 1, has_next = 0.  Every arithmetic step is the same kernel on the same
+// operands whatever the partition, so states are bitwise identical for any number of ranks.
+
+// FCF part A -- launches s = 0..c-2: first F sweep (block k's rows from its old C row), then the
+// C step of every block k >= 1 from the first-sweep F row kc-1 (and, with has_next, the outgoing
+// value U[L] = 0 + (U[L-1] + h F(U[L-1])) for the next rank's first C row).  Each C row's old value
+// is consumed at s = 0, before the C step overwrites it at s = c-1; without has_next the last
+// block's first sweep is dead in the reference (overwritten, never read) and is skipped.
+int local_fcf_a(const lmg_system& S, int B, int c, double* U, const double* src, int mode,
+                bool is_first, bool has_next, cudaStream_t st) {
   const int64_t BQ = (int64_t)B * S.width;
   const int nb = S.num_layers / c;
-  for (int s = 0; s + 1 < c; ++s) {  // first F sweep of blocks 0..nb-2
+  const int K1 = nb - 1 + (has_next ? 1 : 0);
+  for (int s = 0; s + 1 < c; ++s) {
     Fam f;
-    f.ntasks = nb - 1; f.blk0 = s; f.blk_step = c;
+    f.ntasks = K1; f.blk0 = s; f.blk_step = c;
     f.x = U + (int64_t)s * BQ; f.x_ts = c * BQ;
     f.s = src_fam(src, mode, BQ, s + 1); f.s_ts = c * BQ;
     f.out = U + (int64_t)(s + 1) * BQ; f.out_ts = c * BQ;
     TRY(family(S, B, E_PROP, f, st));
   }
-  TRY(c_step(S, B, c, U, src, mode, U + (int64_t)c * BQ, c * BQ, st));
-  TRY(copy_rows(U, 0, src, 0, 1, BQ, st));
-  TRY(f_relax(S, B, c, U, src, mode, st));
-  if (P) TRY(c_step(S, B, c, U, src, mode, P + BQ, BQ, st));
+  Fam f;
+  f.ntasks = K1; f.blk0 = c - 1; f.blk_step = c;
+  f.x = U + (int64_t)(c - 1) * BQ; f.x_ts = c * BQ;
+  f.s = src_fam(src, mode, BQ, c); f.s_ts = c * BQ;
+  f.out = U + (int64_t)c * BQ; f.out_ts = c * BQ;
+  TRY(family(S, B, E_PROP, f, st));
+  if (is_first) TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]
   return LMG_OK;
+}
+
+// FCF part B -- second F sweep of every block, then P[k] = propagate(U[kc-1]) for k = 1..nb-1
+// (+ outgoing P[nb] with has_next): the propagated value of every C row, so the C-row residual is
+// R[kc] = P[k] - U[kc] both before (multigrid.py:208) and after (multigrid.py:228) the correction,
+// which only moves C rows.  With has_next, adv_out = U[(nb-1)c] + H F_H(U[(nb-1)c]) on the coarse
+// system: the next rank's first coarse-source row needs it (network.py:138).
+int local_fcf_b(const lmg_system& S, int B, int c, double* U, const double* src, int mode,
+                double* P, bool has_next, double* adv_out, cudaStream_t st) {
+  const int64_t BQ = (int64_t)B * S.width;
+  const int nb = S.num_layers / c;
+  const int K1 = nb - 1 + (has_next ? 1 : 0);
+  TRY(f_relax(S, B, c, U, src, mode, st));
+  if (P) {
+    Fam f;
+    f.ntasks = K1; f.blk0 = c - 1; f.blk_step = c;
+    f.x = U + (int64_t)(c - 1) * BQ; f.x_ts = c * BQ;
+    f.s = src_fam(src, mode, BQ, c); f.s_ts = c * BQ;
+    f.out = P + BQ; f.out_ts = BQ;
+    TRY(family(S, B, E_PROP, f, st));
+  }
+  if (has_next && adv_out) {
+    const lmg_system Sc = coarsen(S, c);
+    Fam f;
+    f.ntasks = 1; f.blk0 = nb - 1;
+    f.x = U + (int64_t)(nb - 1) * c * BQ;
+    f.out = adv_out;
+    TRY(family(Sc, B, E_ADV, f, st));
+  }
+  return LMG_OK;
+}
+
+// plain FCF on a whole level (multigrid.py:160-172)
+int fcf(const lmg_system& S, int B, int c, double* U, const double* src, int mode, double* P,
+        cudaStream_t st) {
+  TRY(local_fcf_a(S, B, c, U, src, mode, true, false, st));
+  return local_fcf_b(S, B, c, U, src, mode, P, false, nullptr, st);
+}
+
+// coarse FAS source S_H = L_H(U_H) + R_H (multigrid.py:209-212), fused with the injection copy
+// V = U[::c] the recursion edits.  Row 0: S_H[0] = U[0] + (f[0] - U[0]) on the first rank, else
+// (U[0] - adv_in) + (P[0] - U[0]) with the previous rank's adv.
+int local_coarse_source(const lmg_system& S, int B, int c, const double* U, const double* src,
+                        int mode, const double* P, const double* adv_in, bool is_first, double* SH,
+                        double* V, cudaStream_t st) {
+  const int64_t BQ = (int64_t)B * S.width;
+  const int nb = S.num_layers / c;
+  const lmg_system Sc = coarsen(S, c);
+  Fam f;
+  f.ntasks = nb - 1; f.blk0 = 0; f.blk_step = 1;  // coarse block n-1 == fine block (n-1)c
+  f.x = U; f.x_ts = c * BQ;
+  f.y = U + (int64_t)c * BQ; f.y_ts = c * BQ;
+  f.p = P + BQ; f.p_ts = BQ;
+  f.out = SH + BQ; f.out_ts = BQ;
+  f.out2 = V ? V + BQ : nullptr; f.out2_ts = BQ;
+  TRY(family(Sc, B, E_COARSE, f, st));
+  if (is_first) {
+    TRY(launch(CLS_ELEM, 0.0, 24.0 * BQ, st, [&] {
+      k_row0_coarse<<<grid_for(BQ), 256, 0, st>>>(U, src, SH, V, BQ);
+    }));
+  } else {
+    TRY(launch(CLS_ELEM, 0.0, 32.0 * BQ, st, [&] {
+      k_row0_coarse_halo<<<grid_for(BQ), 256, 0, st>>>(U, adv_in, P, SH, V, BQ);
+    }));
+  }
+  return LMG_OK;
+}
+
+int local_correct(int nb, int B, int q, int c, double* U, const double* V, cudaStream_t st) {
+  const int64_t BQ = (int64_t)B * q;
+  return launch(CLS_ELEM, 0.0, 24.0 * nb * BQ, st, [&] {
+    k_correct<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, c * BQ, V, BQ, nb, BQ);
+  });
+}
+
+// partial-sum scratch of the local residuals (doubles)
+size_t local_part_doubles(int L, int B, int q) {
+  const size_t nt = (size_t)((q + TSmall::BN - 1) / TSmall::BN);
+  return (size_t)L * nt * B + 2 * (size_t)L * B + 2 * (size_t)B + (size_t)B * q + 64;
+}
+
+// residual after the correction (multigrid.py:228): C rows elementwise from P, rows kc+1 by
+// the step GEMM, everything else exactly zero.  Writes canonical per-block partials nb x B.
+int local_residual_post(const lmg_system& S, int B, int c, const double* U, const double* src,
+                        int mode, const double* P, bool is_first, double* block_part, double* work,
+                        cudaStream_t st) {
+  const int q = S.width;
+  const int64_t BQ = (int64_t)B * q;
+  const int nb = S.num_layers / c;
+  const int nt = n_tiles(q);
+  double* fpart = work;
+  double* cpart = work + (size_t)nb * nt * B;
+  TRY(launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
+    k_cpart<<<dim3(B, nb), 256, 0, st>>>(U, P, src, is_first ? 1 : 0, c, B, q, cpart);
+  }));
+  Fam f;  // rows kc+1, k = 0..nb-1
+  f.ntasks = nb; f.blk0 = 0; f.blk_step = c;
+  f.x = U; f.x_ts = c * BQ;
+  f.s = src_fam(src, mode, BQ, 1); f.s_ts = c * BQ;
+  f.y = U + BQ; f.y_ts = c * BQ;
+  f.part = fpart; f.slot0 = 0;
+  TRY(family(S, B, E_RESID, f, st));
+  return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
+    k_combine_post<<<(int)(((int64_t)nb * B + 255) / 256), 256, 0, st>>>(cpart, fpart, nb, nt, B,
+                                                                          block_part);
+  });
+}
+
+// full residual, part a: rows 1..L-1 (+ the outgoing adv of row L with has_next)
+int local_residual_full_a(const lmg_system& S, int B, const double* U, const double* src, int mode,
+                          bool has_next, double* adv_out, double* work, cudaStream_t st) {
+  const int64_t BQ = (int64_t)B * S.width;
+  const int L = S.num_layers;
+  Fam f;
+  f.ntasks = L - 1; f.blk0 = 0; f.blk_step = 1;
+  f.x = U; f.x_ts = BQ;
+  f.s = src_fam(src, mode, BQ, 1); f.s_ts = BQ;
+  f.y = U + BQ; f.y_ts = BQ;
+  f.part = work; f.slot0 = n_tiles(S.width);  // row j's tiles at slot j*nt
+  TRY(family(S, B, E_RESID, f, st));
+  if (has_next && adv_out) {
+    Fam g;
+    g.ntasks = 1; g.blk0 = L - 1;
+    g.x = U + (int64_t)(L - 1) * BQ;
+    g.out = adv_out;
+    TRY(family(S, B, E_ADV, g, st));
+  }
+  return LMG_OK;
+}
+
+// full residual, part b: row 0 (f[0] - U[0] on the first rank, (f[0] + adv_in) - U[0] elsewhere)
+// and the canonical block partials
+int local_residual_full_b(const lmg_system& S, int B, int c, const double* U, const double* src,
+                          int mode, const double* adv_in, bool is_first, double* block_part,
+                          double* work, cudaStream_t st) {
+  const int q = S.width;
+  const int64_t BQ = (int64_t)B * q;
+  const int L = S.num_layers;
+  const int nb = L / c;
+  const int nt = n_tiles(q);
+  double* rpart = work;
+  double* r0part = work + (size_t)L * nt * B;
+  double* tmp = r0part + 2 * (size_t)B;  // one (B, q) row: f[0] + adv_in
+  const double* s0 = src;
+  if (!is_first) {
+    double* row = reinterpret_cast<double*>(tmp);
+    TRY(launch(CLS_ELEM, 0.0, 24.0 * BQ, st, [&] {
+      k_halo_finish<<<grid_for(BQ), 256, 0, st>>>(src, adv_in, row, BQ);
+    }));
+    s0 = row;
+  }
+  TRY(launch(CLS_ELEM, 0.0, 16.0 * BQ, st, [&] {
+    k_resid_row0<<<B, 256, 0, st>>>(s0, U, nullptr, r0part, 0, B, q);
+  }));
+  return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
+    k_combine_full<<<(int)(((int64_t)nb * B + 255) / 256), 256, 0, st>>>(rpart, r0part, nb, c, nt, B,
+                                                                          block_part);
+  });
 }
 
 // full residual (all rows) -> optional R, per-sample partials from slot 0
@@ -475,32 +722,6 @@ int residual_full(const lmg_system& S, int B, const double* U, const double* src
   f.part = part; f.slot0 = 1;
   TRY(family(S, B, E_RESID, f, st));
   *nslots = 1 + (int64_t)(n - 1) * n_tiles(q);
-  return LMG_OK;
-}
-
-// residual after the C correction: only rows {kc, kc+1} can be nonzero (plus row 0)
-int residual_post(const lmg_system& S, int B, int c, const double* U, const double* src, int mode,
-                  double* part, cudaStream_t st, int64_t* nslots) {
-  const int q = S.width;
-  const int64_t BQ = (int64_t)B * q;
-  const int nb = S.num_layers / c;
-  const int nt = n_tiles(q);
-  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_resid_row0<<<B, 256, 0, st>>>(src, U, nullptr, part, 0, B, q); }));
-  Fam f1;  // rows kc, k = 1..nb-1
-  f1.ntasks = nb - 1; f1.blk0 = c - 1; f1.blk_step = c;
-  f1.x = U + (int64_t)(c - 1) * BQ; f1.x_ts = c * BQ;
-  f1.s = src_fam(src, mode, BQ, c); f1.s_ts = c * BQ;
-  f1.y = U + (int64_t)c * BQ; f1.y_ts = c * BQ;
-  f1.part = part; f1.slot0 = 1;
-  TRY(family(S, B, E_RESID, f1, st));
-  Fam f2;  // rows kc+1, k = 0..nb-1
-  f2.ntasks = nb; f2.blk0 = 0; f2.blk_step = c;
-  f2.x = U; f2.x_ts = c * BQ;
-  f2.s = src_fam(src, mode, BQ, 1); f2.s_ts = c * BQ;
-  f2.y = U + BQ; f2.y_ts = c * BQ;
-  f2.part = part; f2.slot0 = 1 + (int64_t)(nb - 1) * nt;
-  TRY(family(S, B, E_RESID, f2, st));
-  *nslots = 1 + (int64_t)(2 * nb - 1) * nt;
   return LMG_OK;
 }
 
@@ -528,7 +749,8 @@ int levels_for(int n, int c, int threshold, std::vector<int>* sizes) {
 
 struct Workspace {
   std::vector<double*> P, SH, V;  // per relaxed level l: P[l]; per coarse level l+1: SH, V
-  double* part = nullptr;
+  double* part = nullptr;         // residual partial-sum scratch
+  double* block_part = nullptr;   // canonical per-block partials (N/c x B)
   double* norms = nullptr;
   size_t bytes = 0;
 };
@@ -549,56 +771,59 @@ int layout_ws(const lmg_system& fine, int nlevels, int c, int B, char* base, Wor
   int n = fine.num_layers;
   for (int l = 0; l + 1 < nlevels; ++l) {
     int nb = n / c;
-    ws->P[l] = take((size_t)nb * BQ);
+    ws->P[l] = take((size_t)(nb + 1) * BQ);
     ws->SH[l + 1] = take((size_t)nb * BQ);
     ws->V[l + 1] = take((size_t)nb * BQ);
     n = nb;
   }
-  ws->part = take(part_slots(fine.num_layers, fine.width) * (size_t)B);
+  ws->part = take(local_part_doubles(fine.num_layers, B, fine.width));
+  ws->block_part = take((size_t)(fine.num_layers / c + 1) * B);
   ws->norms = take((size_t)B);
   ws->bytes = off;
   return LMG_OK;
 }
 
-// multigrid.py:175-228.  `want_norm` only at the finest level: the recursive call's return value
-// is discarded by the reference (multigrid.py:218-226).
+int norms_from_blocks(const double* block_part, int nblocks, int B, double* norms, cudaStream_t st) {
+  return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
+    k_reduce_norms<<<(B + 127) / 128, 128, 0, st>>>(block_part, nblocks, B, norms);
+  });
+}
+
+// residual norms of a whole level from the initial iterate (multigrid.py:293), canonical order
+int full_norms(const lmg_system& S, int B, int c, const double* U, const double* src, int mode,
+               const Workspace& ws, double* norms, cudaStream_t st) {
+  if (S.num_layers % c) c = S.num_layers;  // single-level hierarchy of indivisible depth: 1 block
+  TRY(local_residual_full_a(S, B, U, src, mode, false, nullptr, ws.part, st));
+  TRY(local_residual_full_b(S, B, c, U, src, mode, nullptr, true, ws.block_part, ws.part, st));
+  return norms_from_blocks(ws.block_part, S.num_layers / c, B, norms, st);
+}
+
+// multigrid.py:175-228 on one GPU.  `want_norm` only at the finest level: the recursive call's
+// return value is discarded by the reference (multigrid.py:218-226).
 int cycle(const lmg_system& S, int nlevels, int l, int c, int B, double* U, const double* src,
           int mode, const Workspace& ws, bool want_norm, double* norms, cudaStream_t st) {
-  const int64_t BQ = (int64_t)B * S.width;
-  int64_t nslots = 0;
   if (l == nlevels - 1) {  // single-level hierarchy: exact solve
     TRY(seq_forward(S, B, src, mode, U, st));
-    if (want_norm) {
-      TRY(residual_full(S, B, U, src, mode, nullptr, ws.part, st, &nslots));
-      TRY(reduce_norms(ws.part, nslots, B, norms, st));
-    }
+    if (want_norm) TRY(full_norms(S, B, c, U, src, mode, ws, norms, st));
     return LMG_OK;
   }
   const int nb = S.num_layers / c;
-  TRY(fcf(S, B, c, U, src, mode, ws.P[l], st));
+  double* P = ws.P[l];
+  TRY(local_fcf_a(S, B, c, U, src, mode, true, false, st));
+  TRY(local_fcf_b(S, B, c, U, src, mode, P, false, nullptr, st));
   const lmg_system Sc = coarsen(S, c);
   const bool coarsest = (l + 1 == nlevels - 1);
   double* SH = ws.SH[l + 1];
   double* V = ws.V[l + 1];
-  {  // coarse FAS source S_H = L_H(U_H) + R_H, fused with the injection copy V = U[::c]
-    Fam f;
-    f.ntasks = nb - 1; f.blk0 = 0; f.blk_step = 1;  // coarse block n-1 == fine block (n-1)c
-    f.x = U; f.x_ts = c * BQ;
-    f.y = U + (int64_t)c * BQ; f.y_ts = c * BQ;
-    f.p = ws.P[l] + BQ; f.p_ts = BQ;
-    f.out = SH + BQ; f.out_ts = BQ;
-    f.out2 = coarsest ? nullptr : V + BQ; f.out2_ts = BQ;
-    TRY(family(Sc, B, E_COARSE, f, st));
-    TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_row0_coarse<<<grid_for(BQ), 256, 0, st>>>(U, src, SH, coarsest ? nullptr : V, BQ); }));
-  }
+  TRY(local_coarse_source(S, B, c, U, src, mode, P, nullptr, true, SH, coarsest ? nullptr : V, st));
   if (coarsest)
     TRY(seq_forward(Sc, B, SH, LMG_SRC_DENSE, V, st));
   else
     TRY(cycle(Sc, nlevels, l + 1, c, B, V, SH, LMG_SRC_DENSE, ws, false, nullptr, st));
-  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_correct<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, c * BQ, V, BQ, nb, BQ); }));
+  TRY(local_correct(nb, B, S.width, c, U, V, st));
   if (want_norm) {
-    TRY(residual_post(S, B, c, U, src, mode, ws.part, st, &nslots));
-    TRY(reduce_norms(ws.part, nslots, B, norms, st));
+    TRY(local_residual_post(S, B, c, U, src, mode, P, true, ws.block_part, ws.part, st));
+    TRY(norms_from_blocks(ws.block_part, nb, B, norms, st));
   }
   return LMG_OK;
 }
@@ -792,9 +1017,7 @@ int lmg_solve(const lmg_system* fine, int nlevels, int c, int B, double* states,
   const int64_t BQ = (int64_t)B * q;
 
   if (!use_initial) TRY(copy_rows(states, BQ, src, 0, n, BQ, st));  // initial_guess: tile(f[0])
-  int64_t nslots = 0;
-  TRY(residual_full(*fine, B, states, src, src_mode, nullptr, ws.part, st, &nslots));
-  TRY(reduce_norms(ws.part, nslots, B, ws.norms, st));
+  TRY(full_norms(*fine, B, c, states, src, src_mode, ws, ws.norms, st));
 
   std::vector<double> nrm(B);
   CUDA_TRY(cudaMemcpyAsync(nrm.data(), ws.norms, B * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -882,6 +1105,79 @@ int lmg_param_grads(const lmg_system* fine, int B, const double* states, const d
                                                          fine->step, scale, lr, gb,
                                                          const_cast<double*>(fine->b), fine->b_stride); }));
   return LMG_OK;
+}
+
+// ---- partition-aware level operations (include/lmg.h "layer-partitioned" section) ----------
+
+int lmg_local_fcf_a(const lmg_system* sys, int B, int c, double* U, const double* src,
+                    int src_mode, int is_first, int has_next, void* stream) {
+  TRY(check_sys(sys, B));
+  TRY(check_levels(*sys, 2, c));
+  return local_fcf_a(*sys, B, c, U, src, src_mode, is_first != 0, has_next != 0, S_(stream));
+}
+
+int lmg_local_fcf_b(const lmg_system* sys, int B, int c, double* U, const double* src,
+                    int src_mode, double* P, int has_next, double* adv_out, void* stream) {
+  TRY(check_sys(sys, B));
+  TRY(check_levels(*sys, 2, c));
+  return local_fcf_b(*sys, B, c, U, src, src_mode, P, has_next != 0, adv_out, S_(stream));
+}
+
+int lmg_halo_finish(const double* s0, const double* adv_in, double* out, int64_t len, void* stream) {
+  cudaStream_t st = S_(stream);
+  return launch(CLS_ELEM, 0.0, 24.0 * len, st, [&] {
+    k_halo_finish<<<grid_for(len), 256, 0, st>>>(s0, adv_in, out, len);
+  });
+}
+
+int lmg_local_coarse_source(const lmg_system* sys, int B, int c, const double* U,
+                            const double* src, int src_mode, const double* P,
+                            const double* adv_in, int is_first, double* SH, double* V,
+                            void* stream) {
+  TRY(check_sys(sys, B));
+  TRY(check_levels(*sys, 2, c));
+  if (!is_first && !adv_in) return fail(LMG_ERR_PROTOCOL, "non-first rank needs the previous rank's adv row");
+  return local_coarse_source(*sys, B, c, U, src, src_mode, P, adv_in, is_first != 0, SH, V, S_(stream));
+}
+
+int lmg_local_correct(int n_blocks, int B, int q, int c, double* U, const double* V, void* stream) {
+  return local_correct(n_blocks, B, q, c, U, V, S_(stream));
+}
+
+size_t lmg_local_workspace(int L, int B, int q) {
+  return local_part_doubles(L, B, q) * sizeof(double);
+}
+
+int lmg_local_residual_post(const lmg_system* sys, int B, int c, const double* U,
+                            const double* src, int src_mode, const double* P, int is_first,
+                            double* block_part, void* work, void* stream) {
+  TRY(check_sys(sys, B));
+  TRY(check_levels(*sys, 2, c));
+  return local_residual_post(*sys, B, c, U, src, src_mode, P, is_first != 0, block_part,
+                             reinterpret_cast<double*>(work), S_(stream));
+}
+
+int lmg_local_residual_full_a(const lmg_system* sys, int B, const double* U, const double* src,
+                              int src_mode, int has_next, double* adv_out, void* work,
+                              void* stream) {
+  TRY(check_sys(sys, B));
+  return local_residual_full_a(*sys, B, U, src, src_mode, has_next != 0, adv_out,
+                               reinterpret_cast<double*>(work), S_(stream));
+}
+
+int lmg_local_residual_full_b(const lmg_system* sys, int B, int c, const double* U,
+                              const double* src, int src_mode, const double* adv_in, int is_first,
+                              double* block_part, void* work, void* stream) {
+  TRY(check_sys(sys, B));
+  if (sys->num_layers % c) return fail(LMG_ERR_CONFIGURATION, "rank's layers are not whole blocks");
+  if (!is_first && !adv_in) return fail(LMG_ERR_PROTOCOL, "non-first rank needs the previous rank's adv row");
+  return local_residual_full_b(*sys, B, c, U, src, src_mode, adv_in, is_first != 0, block_part,
+                               reinterpret_cast<double*>(work), S_(stream));
+}
+
+int lmg_norms_from_blocks(const double* block_part, int nblocks, int B, double* norms,
+                          void* stream) {
+  return norms_from_blocks(block_part, nblocks, B, norms, S_(stream));
 }
 
 int lmg_dense_apply(const double* W, const double* b, int act, int M, int q_out, int q_in,

@@ -1,0 +1,422 @@
+"""Layer-parallel FAS across GPUs: the reference's worker partition (parallel.py:61-79) mapped to
+ranks, one process per GPU, halos over NCCL (NVLink) via torch.distributed.
+
+Each rank owns a contiguous run of whole blocks at every relaxed level (requires
+N_l % (world * c) == 0 for every relaxed level l -- the reference's assignment k // ceil(nb/P) is
+then an equal split) and the matching rows of the coarsest level.  Per cycle and cross edge:
+
+  after FCF part A : U[L]            1 row   (the reference's one BoundaryMessage per edge per
+                                              C-sweep, parallel.py:183-216)
+  after FCF part B : P[nb], adv_out  2 rows  (C-row residual and coarse-source halo)
+  coarsest level   : the exact forward substitution is rank-pipelined: each rank solves its rows
+                     and hands its last state to the next (1 row); no theta or grid gather
+  norms            : all_gather of per-block partials (B doubles per block), summed in global
+                     block order -> bitwise the single-GPU norms.
+
+States are bitwise identical to the single-GPU solve for any world size (same kernels on the same
+operands); tests/test_distributed.py checks that under gloo with an oracle-backed backend.
+
+The adjoint system runs the same machinery in reverse rank order (its first block is the last
+layer, training.py:216-224).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from ._arrays import require_cuda
+from .errors import ConfigurationError
+
+
+class CudaOps:
+    """Local level operations through liblmg.so (device tensors)."""
+
+    name = "cuda"
+
+    def __init__(self, device):
+        self.device = device
+
+    def _st(self):
+        return _lib.stream_handle(self.device)
+
+    @staticmethod
+    def _p(t):
+        return None if t is None else t.data_ptr()
+
+    def fcf_a(self, lv, U, S, smode, is_first, has_next):
+        _lib.call("lmg_local_fcf_a", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
+                  int(is_first), int(has_next), self._st())
+
+    def fcf_b(self, lv, U, S, smode, P, has_next, adv_out):
+        _lib.call("lmg_local_fcf_b", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
+                  P.data_ptr(), int(has_next), self._p(adv_out), self._st())
+
+    def halo_finish(self, s0, adv, out):
+        _lib.call("lmg_halo_finish", self._p(s0), adv.data_ptr(), out.data_ptr(), out.numel(),
+                  self._st())
+
+    def coarse_source(self, lv, U, S, smode, P, adv_in, is_first, SH, V):
+        _lib.call("lmg_local_coarse_source", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
+                  P.data_ptr(), self._p(adv_in), int(is_first), SH.data_ptr(), self._p(V),
+                  self._st())
+
+    def correct(self, lv, U, V):
+        _lib.call("lmg_local_correct", lv.nb, lv.B, lv.q, lv.c, U.data_ptr(), V.data_ptr(), self._st())
+
+    def residual_post(self, lv, U, S, smode, P, is_first, block_part, work):
+        _lib.call("lmg_local_residual_post", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
+                  P.data_ptr(), int(is_first), block_part.data_ptr(), work.data_ptr(), self._st())
+
+    def residual_full_a(self, lv, U, S, smode, has_next, adv_out, work):
+        _lib.call("lmg_local_residual_full_a", lv.desc(), lv.B, U.data_ptr(), self._p(S), smode,
+                  int(has_next), self._p(adv_out), work.data_ptr(), self._st())
+
+    def residual_full_b(self, lv, U, S, smode, adv_in, is_first, block_part, work):
+        _lib.call("lmg_local_residual_full_b", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
+                  self._p(adv_in), int(is_first), block_part.data_ptr(), work.data_ptr(), self._st())
+
+    def norms_from_blocks(self, block_part, nblocks, B, norms):
+        _lib.call("lmg_norms_from_blocks", block_part.data_ptr(), nblocks, B, norms.data_ptr(),
+                  self._st())
+
+    def propagate(self, lv, u_start, S, smode, start, stop, out):
+        _lib.call("lmg_propagate", lv.desc(), lv.B, u_start.data_ptr(), self._p(S), smode, start, stop,
+                  out.data_ptr(), self._st())
+
+    def adv_last(self, lv, U, out):
+        """out = U[L-1] + h F_{L-1}(U[L-1]) (no source)."""
+        _lib.call("lmg_propagate", lv.desc(), lv.B, U[lv.L - 1].data_ptr(), None, _lib.SRC_HEAD,
+                  lv.L, lv.L + 1, out.data_ptr(), self._st())
+
+    def work_doubles(self, L, B, q):
+        return _lib.load().lmg_local_workspace(L, B, q) // 8 + 1
+
+
+class LocalLevel:
+    """This rank's view of one level: L local layers (nb blocks) of a system view."""
+
+    def __init__(self, view, c, B, adjoint_D=None):
+        self.view, self.c, self.B = view, c, B
+        self.L = view.n
+        self.q = view.width
+        self.nb = self.L // c if c else 0
+        self.adjoint_D = adjoint_D
+        self.step = view.step
+
+    def desc(self):
+        return self.view.desc(self.adjoint_D)
+
+    def coarsen(self):
+        return LocalLevel(self.view.coarsen(self.c), self.c, self.B, self.adjoint_D)
+
+
+def check_partition(N, c, nlevels, world):
+    """Every relaxed level must split into whole blocks, equally over the ranks."""
+    n = N
+    for _ in range(nlevels - 1):
+        if n % (world * c):
+            raise ConfigurationError(
+                f"layer-partitioned solve needs every relaxed level divisible by world*c; "
+                f"level with {n} layers, world {world}, c {c}")
+        n //= c
+    if n % world:
+        raise ConfigurationError(f"coarsest level of {n} layers does not split over {world} ranks")
+
+
+class DistSolver:
+    """FAS solve of a layer-partitioned system (forward or adjoint) on this rank."""
+
+    def __init__(self, view_local, N_total, c, nlevels, B, *, rank, world, ops, reverse=False,
+                 adjoint_D=None, device=None, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank, self.world = rank, world
+        self.reverse = reverse
+        # position along the system's layer order: forward rank r, adjoint world-1-r
+        self.pos = world - 1 - rank if reverse else rank
+        self.prev = None if self.pos == 0 else (rank + 1 if reverse else rank - 1)
+        self.next = None if self.pos == world - 1 else (rank - 1 if reverse else rank + 1)
+        self.is_first = self.pos == 0
+        self.has_next = self.next is not None
+        self.c, self.nlevels, self.B = c, nlevels, B
+        self.N_total = N_total
+        check_partition(N_total, c, nlevels, world)
+        self.ops = ops
+        t = require_cuda() if ops.name == "cuda" else __import__("torch")
+        self.t = t
+        self.device = device
+        lv = LocalLevel(view_local, c, B, adjoint_D)
+        self.levels = [lv]
+        for _ in range(nlevels - 1):
+            self.levels.append(self.levels[-1].coarsen())
+        q = lv.q
+        f64 = dict(dtype=t.float64, device=device)
+        z = lambda *s: t.zeros(*s, **f64)  # noqa: E731
+        self.U, self.S, self.P = [], [], []
+        for l, lev in enumerate(self.levels):
+            L = lev.L
+            self.U.append(z(L + 1, B, q) if l > 0 else None)   # level 0 states are the caller's
+            self.S.append(z(L + 1, B, q) if l > 0 else None)   # coarse sources, zero row L
+            self.P.append(z(lev.nb + 2, B, q) if l < nlevels - 1 else None)  # + [P_out, adv_out]
+        self.recv1 = z(1, B, q)
+        self.recv2 = z(2, B, q)
+        self.work = z(ops.work_doubles(lv.L + 1, B, q))
+        nbt = N_total // c
+        self.block_part = z(lv.nb + 1, B)
+        self.block_all = z(world * (lv.nb + 1), B)
+        self.norms = z(B)
+        self.nblocks_total = nbt
+        self.messages = 0  # halo messages sent by this rank (protocol accounting)
+
+    # -- point-to-point halo: send `send` to next, receive into `recv` from prev -------------------
+    def _host_staged(self):
+        """gloo moves only host tensors: stage device halos through host memory (used to run
+        several ranks on one GPU in tests; NCCL moves device memory directly over NVLink)."""
+        return self.world > 1 and self.dist.get_backend(self.group) == "gloo" and self.ops.name == "cuda"
+
+    def _exchange(self, send, recv):
+        dist = self.dist
+        stage = self._host_staged()
+        ops = []
+        if self.has_next and send is not None:
+            buf = send.contiguous().cpu() if stage else send.contiguous()
+            ops.append(dist.P2POp(dist.isend, buf, self.next, group=self.group))
+            self.messages += 1
+        rbuf = None
+        if not self.is_first and recv is not None:
+            rbuf = recv.cpu() if stage else recv
+            ops.append(dist.P2POp(dist.irecv, rbuf, self.prev, group=self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        if stage and rbuf is not None:
+            recv.copy_(rbuf)
+
+    def _gather_norms(self, lev, block_part):
+        dist = self.dist
+        nb = lev.nb
+        if self._host_staged():
+            loc = block_part[:nb].cpu()
+            parts = [self.t.empty_like(loc) for _ in range(self.world)]
+            dist.all_gather(parts, loc, group=self.group)
+            parts = [p.to(block_part.device) for p in parts]
+        else:
+            parts = [self.t.empty_like(block_part[:nb]) for _ in range(self.world)]
+            dist.all_gather(parts, block_part[:nb].contiguous(), group=self.group)
+        order = range(self.world - 1, -1, -1) if self.reverse else range(self.world)
+        allp = self.t.cat([parts[r] for r in order], 0)
+        self.ops.norms_from_blocks(allp, allp.shape[0], self.B, self.norms)
+        return self.norms
+
+    # -- the level-0 residual from the initial iterate (multigrid.py:293) ---------------------
+    def initial_norms(self, U0, S0, smode):
+        lev = self.levels[0]
+        adv = self.P[0][lev.nb + 1 : lev.nb + 2] if self.has_next else None
+        self.ops.residual_full_a(lev, U0, S0, smode, self.has_next, adv, self.work)
+        self._exchange(adv, self.recv1)
+        self.ops.residual_full_b(lev, U0, S0, smode, None if self.is_first else self.recv1[0],
+                                 self.is_first, self.block_part, self.work)
+        return self._gather_norms(lev, self.block_part)
+
+    # -- rank-pipelined exact solve of the coarsest level (network.py:111-123) ----------------
+    def _coarsest(self, l, V, SH):
+        lev = self.levels[l]
+        ops = self.ops
+        if self.is_first:
+            V[0].copy_(SH[0])
+        else:
+            self._exchange(None, self.recv1)
+            ops.halo_finish(SH[0], self.recv1[0], V[0])
+        if lev.L > 1:
+            ops.propagate(lev, V[0], SH, _lib.SRC_DENSE, 1, lev.L, V[1 : lev.L])
+        if self.has_next:
+            ops.adv_last(lev, V, self.recv2[0:1])
+            self._exchange(self.recv2[0:1], None)
+
+    # -- one FAS cycle at level l (multigrid.py:175-228) --------------------------------------
+    def cycle(self, l, U, S, smode, want_norm):
+        lev = self.levels[l]
+        ops = self.ops
+        nb, c = lev.nb, self.c
+        P = self.P[l]
+        ops.fcf_a(lev, U, S, smode, self.is_first, self.has_next)
+        self._exchange(U[lev.L : lev.L + 1] if self.has_next else None, self.recv1)
+        if not self.is_first:
+            ops.halo_finish(None if S is None else S[0], self.recv1[0], U[0])
+        adv_out = P[nb + 1] if self.has_next else None
+        ops.fcf_b(lev, U, S, smode, P, self.has_next, adv_out)
+        self._exchange(P[nb : nb + 2] if self.has_next else None, self.recv2)
+        if not self.is_first:
+            ops.halo_finish(None if S is None else S[0], self.recv2[0], P[0])
+        Vn, SHn = self.U[l + 1], self.S[l + 1]
+        coarsest = l + 1 == self.nlevels - 1
+        ops.coarse_source(lev, U, S, smode, P, None if self.is_first else self.recv2[1],
+                          self.is_first, SHn, None if coarsest else Vn)
+        if coarsest:
+            self._coarsest(l + 1, Vn, SHn)
+        else:
+            self.cycle(l + 1, Vn, SHn, _lib.SRC_DENSE, False)
+        ops.correct(lev, U, Vn)
+        if want_norm:
+            ops.residual_post(lev, U, S, smode, P, self.is_first, self.block_part, self.work)
+            return self._gather_norms(lev, self.block_part)
+        return None
+
+    def solve(self, U0, S0, smode, *, tol, max_cycles, use_initial=False):
+        """multigrid.py:263-311 per sample on the partitioned system.  U0: this rank's level-0
+        states (L+1 rows; row L is scratch), S0: head (B, q) on the first rank / None, or dense.
+        Returns (hist (max_cycles+1, B), cycles (B,), converged (B,)), identical on every rank."""
+        t = self.t
+        B = self.B
+        L = self.levels[0].L
+        if not use_initial:
+            if self.is_first:
+                U0[:L].copy_(S0[0] if smode == _lib.SRC_DENSE else S0)
+            else:
+                # initial_guess tiles source row 0 of the FIRST rank (multigrid.py:257-260)
+                pass
+            self._broadcast_head(U0, S0, smode)
+        nrm = self.initial_norms(U0, S0, smode).cpu().numpy()
+        hist = np.full((max_cycles + 1, B), np.nan)
+        hist[0] = nrm
+        cyc = np.zeros(B, dtype=np.int32)
+        done = nrm <= tol
+        parked = {}
+        for b in np.nonzero(done)[0]:
+            if not done.all():
+                parked[int(b)] = U0[:L, int(b)].clone()
+        k = 0
+        while not done.all() and k < max_cycles:
+            nrm = self.cycle(0, U0, S0, smode, True).cpu().numpy()
+            k += 1
+            for b in range(B):
+                if done[b]:
+                    continue
+                hist[k, b] = nrm[b]
+                cyc[b] = k
+                if nrm[b] <= tol:
+                    done[b] = True
+            if not done.all():
+                for b in np.nonzero(done)[0]:
+                    if int(b) not in parked:
+                        parked[int(b)] = U0[:L, int(b)].clone()
+        for b, v in parked.items():
+            U0[:L, b].copy_(v)
+        return hist[: k + 1], cyc, done.copy()
+
+    def _broadcast_head(self, U0, S0, smode):
+        """initial_guess needs source row 0 (the opened input) on every rank."""
+        L = self.levels[0].L
+        head = S0[0] if (self.is_first and smode == _lib.SRC_DENSE) else S0
+        if self.world > 1:
+            buf = head.contiguous() if self.is_first else self.t.empty_like(U0[0])
+            src_rank = self.world - 1 if self.reverse else 0
+            if self._host_staged():
+                hb = buf.cpu()
+                self.dist.broadcast(hb, src=src_rank, group=self.group)
+                buf = hb.to(U0.device)
+            else:
+                self.dist.broadcast(buf, src=src_rank, group=self.group)
+            head = buf
+        U0[:L].copy_(head.expand_as(U0[:L]))
+
+
+# ---------------------------------------------------------------------------------------------
+# training step over ranks
+
+
+class LayerParallelTrainer:
+    """The DeviceTrainer step with the layer axis partitioned over all ranks of the default group
+    (one process per GPU).  Each rank generates only its own layers' parameters on device
+    (bitwise the reference's random_network), rank 0 owns the opening, the last rank the readout."""
+
+    def __init__(self, depth, width, seed, *, coarsening=4, threshold=None, tol=1e-9, max_cycles=50,
+                 adjoint="fas", learning_rate=0.1, batch=None):
+        import torch
+        import torch.distributed as dist
+
+        from .multigrid import _levels_for
+        from .synthetic import device_network
+
+        self.t = torch
+        self.dist = dist
+        self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.N, self.q = depth, width
+        self.c = coarsening
+        self.nlevels = _levels_for(depth, coarsening, threshold)
+        check_partition(depth, coarsening, self.nlevels, self.world)
+        L = depth // self.world
+        self.lo = self.rank * L
+        self.dnet = device_network(depth, width, seed, layers=(self.lo, self.lo + L), device=self.device)
+        self.L = L
+        self.tol, self.max_cycles = tol, max_cycles
+        self.adjoint = adjoint
+        self.lr = learning_rate
+        self.ops = CudaOps(self.device)
+        self._fwd = self._adj = None
+        self._B = None
+
+    def _setup(self, B):
+        if self._B == B:
+            return
+        t = self.t
+        from .network import SystemView
+
+        view = SystemView(self.dnet.stack, 1, self.dnet.step_size, self.L)
+        self.U = t.zeros(self.L + 1, B, self.q, dtype=t.float64, device=self.device)
+        self.D = t.zeros(self.L, B, self.q, dtype=t.float64, device=self.device)
+        self.lam = t.zeros(self.L + 1, B, self.q, dtype=t.float64, device=self.device)
+        self._fwd = DistSolver(view, self.N, self.c, self.nlevels, B, rank=self.rank, world=self.world,
+                               ops=self.ops, device=self.device)
+        self._adj = DistSolver(view, self.N, self.c, self.nlevels, B, rank=self.rank, world=self.world,
+                               ops=self.ops, device=self.device, reverse=True, adjoint_D=self.D)
+        self._view = view
+        self._B = B
+
+    def step(self, X, labels):
+        from .training import StepResult, _dense_apply, _dense_vjp, softmax_ce
+
+        t = self.t
+        B = X.shape[0]
+        self._setup(B)
+        st = _lib.stream_handle()
+        first, last = self.rank == 0, self.rank == self.world - 1
+        f0 = _dense_apply(self.dnet.Wo, self.dnet.bo, self.dnet.open_act, X) if first else None
+        hist, cyc, conv = self._fwd.solve(self.U, f0, _lib.SRC_HEAD, tol=self.tol,
+                                          max_cycles=self.max_cycles)
+        view = self._view
+        _lib.call("lmg_act_deriv", view.desc(), B, self.U.data_ptr(), self.D.data_ptr(), st)
+        g_final = loss = None
+        if last:
+            final = t.empty((1, B, self.q), dtype=t.float64, device=self.device)
+            _lib.call("lmg_propagate", view.desc(), B, self.U[self.L - 1].data_ptr(), None,
+                      _lib.SRC_HEAD, self.L, self.L + 1, final.data_ptr(), st)
+            logits = _dense_apply(self.dnet.Wr, self.dnet.br, self.dnet.read_act, final[0])
+            loss, dl = softmax_ce(logits, labels)
+            g_final, gWr, gbr = _dense_vjp(self.dnet.Wr, self.dnet.br, self.dnet.read_act, final[0], dl)
+        if self.adjoint != "fas":
+            raise ConfigurationError("the layer-partitioned trainer runs the FAS adjoint")
+        ahist, acyc, aconv = self._adj.solve(self.lam, g_final, _lib.SRC_HEAD, tol=self.tol,
+                                             max_cycles=self.max_cycles)
+        scale = 1.0 / B
+        if first:  # lambda^0 and the opening gradient
+            lam0 = t.empty((1, B, self.q), dtype=t.float64, device=self.device)
+            _lib.call("lmg_propagate", view.desc(self.D), B, self.lam[self.L - 1].data_ptr(), None,
+                      _lib.SRC_HEAD, self.L, self.L + 1, lam0.data_ptr(), st)
+            _, gWo, gbo = _dense_vjp(self.dnet.Wo, self.dnet.bo, self.dnet.open_act, X, lam0[0],
+                                     want_gx=False)
+        _lib.call("lmg_param_grads", view.desc(), B, self.U.data_ptr(), self.lam.data_ptr(),
+                  self.D.data_ptr(), scale, float(self.lr), None, None, st)
+        if first and self.lr:
+            self.dnet.Wo.sub_(gWo * (scale * self.lr))
+            self.dnet.bo.sub_(gbo * (scale * self.lr))
+        if last and self.lr:
+            self.dnet.Wr.sub_(gWr * (scale * self.lr))
+            self.dnet.br.sub_(gbr * (scale * self.lr))
+        if loss is None:
+            loss = t.zeros(B, dtype=t.float64, device=self.device)
+        return StepResult(loss, hist, cyc, conv, ahist, acyc, aconv)

@@ -1,0 +1,95 @@
+"""The layer-partitioned solver on the GPU through the C-ABI (CudaOps): two ranks sharing the one
+GPU of the test box (gloo, halos staged through host memory), against the single-GPU solve.
+States, residual histories and the SGD-updated parameters must be BITWISE identical: every row is
+produced by the same kernel on the same operands whatever the partition, and norm partials are
+summed per block in global block order."""
+
+import os
+import pickle
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+from _golden import ROOT
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+N, Q, B, C, THR = 256, 64, 8, 4, 16  # levels [256, 64, 16]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _inputs():
+    import paper_2007_07336_b200 as P
+
+    X = P.random_batch(Q, [3, N, Q], B)
+    return X, np.arange(B) % 10
+
+
+def _worker(rank, world, port, out):
+    sys.path.insert(0, ROOT)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    from paper_2007_07336_b200.distributed import LayerParallelTrainer
+
+    X, labels = _inputs()
+    tr = LayerParallelTrainer(N, Q, [3, N, Q], coarsening=C, threshold=THR, tol=1e-10, max_cycles=40,
+                              learning_rate=0.1)
+    res = tr.step(torch.from_numpy(X).cuda(), torch.from_numpy(labels).cuda())
+    U = tr.U[: tr.L].cpu()
+    W = tr.dnet.stack.W.cpu()
+    parts = [torch.empty_like(U) for _ in range(world)]
+    dist.all_gather(parts, U)
+    wparts = [torch.empty_like(W) for _ in range(world)]
+    dist.all_gather(wparts, W)
+    loss = res.loss.cpu()
+    dist.broadcast(loss, src=world - 1)
+    if rank == 0:
+        with open(out, "wb") as fh:
+            pickle.dump(dict(U=torch.cat(parts).numpy(), W=torch.cat(wparts).numpy(), loss=loss.numpy(),
+                             hist=res.fwd_hist, ahist=res.adj_hist, cyc=res.fwd_cycles,
+                             acyc=res.adj_cycles), fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(world, tmp_path):
+    out = str(tmp_path / f"w{world}.pkl")
+    mp.spawn(_worker, args=(world, _port(), out), nprocs=world, join=True)
+    with open(out, "rb") as fh:
+        return pickle.load(fh)
+
+
+def test_partitioned_training_step_bitwise_vs_single_gpu(tmp_path):
+    import paper_2007_07336_b200 as P
+
+    X, labels = _inputs()
+    d = P.device_network(N, Q, [3, N, Q])
+    tr = P.DeviceTrainer(d, coarsening=C, threshold=THR, tol=1e-10, max_cycles=40, adjoint="fas",
+                         learning_rate=0.1)
+    U, hist, cyc, conv = tr.forward(torch.from_numpy(X).cuda())
+    U = U.cpu().numpy().copy()
+    res = tr.step(torch.from_numpy(X).cuda(), torch.from_numpy(labels).cuda())
+    W1 = d.stack.W.cpu().numpy()
+    for world in (1, 2, 4):
+        r = _run(world, tmp_path)
+        assert r["U"].tobytes() == U.tobytes(), world
+        assert np.array_equal(r["hist"], hist[: cyc.max() + 1], equal_nan=True), world
+        assert np.array_equal(r["ahist"], res.adj_hist[: res.adj_cycles.max() + 1], equal_nan=True), world
+        assert r["W"].tobytes() == W1.tobytes(), world
+        assert np.array_equal(r["loss"], res.loss.cpu().numpy()), world
