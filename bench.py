@@ -214,7 +214,12 @@ def fp64_peak_tflops(torch, dev):
 
 def load_traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    import glob
+
+    cands = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
+    if not cands:
+        return None, None
+    p = cands[-1]
     try:
         with open(p) as fh:
             d = json.load(fh)
