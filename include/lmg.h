@@ -180,6 +180,12 @@ int lmg_local_residual_full_b(const lmg_system* sys, int B, int c, const double*
 int lmg_norms_from_blocks(const double* block_part, int nblocks, int B, double* norms,
                           void* stream);
 
+/* kernels.py:139-150 / 153-188 for block j of a system (dense or conv2d): Y = act(F_j(X)), and
+ * the VJP: gX = J_j^T G, batch-summed gW / gb (HWIO for conv).  `work` needs B*q doubles. */
+int lmg_apply_block(const lmg_system* sys, int B, int j, const double* X, double* Y, void* stream);
+int lmg_vjp_block(const lmg_system* sys, int B, int j, const double* X, const double* G, double* gX,
+                  double* gW, double* gb, double* work, void* stream);
+
 /* kernels.py:139-150 apply_transform (dense) for a batch: Y (M, q_out) = act(X W^T + b),
  * X (M, q_in), W (q_out, q_in) row-major, b (q_out) or NULL. */
 int lmg_dense_apply(const double* W, const double* b, int act, int M, int q_out, int q_in,

@@ -85,6 +85,8 @@ SIGNATURES = {
     "lmg_local_residual_full_a": (_I, [_SYS, _I, _P, _P, _I, _I, _P, _P, _P]),
     "lmg_local_residual_full_b": (_I, [_SYS, _I, _I, _P, _P, _I, _P, _I, _P, _P, _P]),
     "lmg_norms_from_blocks": (_I, [_P, _I, _I, _P, _P]),
+    "lmg_apply_block": (_I, [_SYS, _I, _I, _P, _P, _P]),
+    "lmg_vjp_block": (_I, [_SYS, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "lmg_dense_apply": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P]),
     "lmg_dense_vjp": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "lmg_l2_norms": (_I, [_P, _I, _I, _I, _P, _P, _P]),

@@ -26,7 +26,7 @@
 #include <vector>
 
 #include "lmg.h"
-#include "lmg_gemm.cuh"
+#include "lmg_conv.cuh"
 
 using namespace lmg;
 
@@ -229,6 +229,38 @@ __global__ void k_combine_full(const double* __restrict__ rpart, const double* _
   block_part[e] = s;
 }
 
+// conv bias gradient + SGD: gb_n[co] = (h * sum_{b,pix} lam^{n+1}[b][co][pix] D_n[b][co][pix])*scale
+__global__ void k_conv_bias_grads(const double* __restrict__ lam_top, int64_t lam_ts,
+                                  const double* __restrict__ D, int B, int C, int HW, double h,
+                                  double scale, double lr, double* __restrict__ gb,
+                                  double* __restrict__ bias, int64_t b_stride) {
+  __shared__ double sh[256];
+  const int co = blockIdx.x, n = blockIdx.y;
+  const int64_t q = (int64_t)C * HW;
+  const double* L = lam_top + (int64_t)n * lam_ts;
+  const double* Dn = D + (int64_t)n * B * q;
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < (int64_t)B * HW; e += blockDim.x) {
+    const int64_t b = e / HW, p = e - b * HW;
+    const int64_t idx = b * q + (int64_t)co * HW + p;
+    s += __dmul_rn(L[idx], Dn[idx]);
+  }
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if (threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double g = __dmul_rn(__dmul_rn(sh[0], h), scale);
+    if (gb) gb[(int64_t)n * C + co] = g;
+    if (lr != 0.0 && bias) {
+      double* bp = bias + (int64_t)n * b_stride + co;
+      *bp = __dadd_rn(*bp, -__dmul_rn(lr, g));
+    }
+  }
+}
+
 int grid_for(int64_t total) {
   int64_t g = (total + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
@@ -379,15 +411,62 @@ int launch_step(Layout L, const StepArgs& a, cudaStream_t st) {
 // systems
 
 bool is_adjoint(const lmg_system& s) { return s.kind == LMG_DENSE_ADJOINT || s.kind == LMG_CONV_ADJOINT; }
+bool is_conv(const lmg_system& s) { return s.kind == LMG_CONV || s.kind == LMG_CONV_ADJOINT; }
+
+// ---- conv2d (lmg_conv.cuh) -------------------------------------------------------------------
+using CT = ConvTile<32, 64, 16, 2, 2, 4>;  // 32 pixels x 64 channels, warp 16x32
+
+ConvGeom geom_of(const lmg_system& S) {
+  ConvGeom g;
+  g.C = S.channels;
+  g.Cp = (g.C + 31) / 32 * 32;
+  g.H = S.height;
+  g.W = S.px_width;
+  g.HW = g.H * g.W;
+  g.HWp = (g.HW + CT::BM - 1) / CT::BM * CT::BM;
+  g.q = (int64_t)g.C * g.HW;
+  return g;
+}
+
+template <int V>
+int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
+  constexpr int A_SZ = CT::BK * CT::LDA;
+  constexpr int B_SZ = (V == CV_ADJ) ? CT::BN * CT::LDB_K : CT::BK * CT::LDB_MN;
+  constexpr int STAGE = A_SZ * (V == CV_ADJ ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
+  constexpr size_t SMEM = (size_t)CT::STAGES * STAGE * sizeof(double);
+  auto kern = conv_gemm<CT, V>;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    attr = true;
+  }
+  if (a.ntasks > 65535) return fail(LMG_ERR_CONFIGURATION, "too many tasks in one launch");
+  dim3 grid((a.N + CT::BN - 1) / CT::BN, (a.M + CT::BM - 1) / CT::BM, a.ntasks);
+  const int cls = V == CV_FWD ? CLS_GEMM_FWD : (V == CV_ADJ ? CLS_GEMM_ADJ : CLS_GEMM_PG);
+  // algorithmic: 2 * 9 C^2 per pixel per sample (zero padding counted as work, kernels.py:135)
+  const double flops = (double)a.ntasks * 2.0 * 9.0 * g.C * g.C * (double)g.HW *
+                       (V == CV_PGRAD ? (double)(a.K / g.HWp) : (double)(a.M / g.HWp));
+  return launch(cls, flops, 0.0, st, [&] { kern<<<grid, CT::NT, SMEM, st>>>(a, g); });
+}
+
+// residual partial slots per state row (one per CTA tile of a row, canonical per tile config)
+int row_slots(const lmg_system& S) {
+  if (!is_conv(S)) return (S.width + TSmall::BN - 1) / TSmall::BN;
+  const ConvGeom g = geom_of(S);
+  return (g.HWp / CT::BM) * ((g.C + CT::BN - 1) / CT::BN);
+}
 
 int check_sys(const lmg_system* s, int B) {
   if (!s) return fail(LMG_ERR_CONFIGURATION, "null system");
   if (s->num_layers < 1) return fail(LMG_ERR_CONFIGURATION, "a system needs at least one block");
   if (s->width < 1 || B < 1) return fail(LMG_ERR_DIMENSION, "width and batch must be >= 1");
-  if (s->kind == LMG_CONV || s->kind == LMG_CONV_ADJOINT)
-    return fail(LMG_ERR_CONFIGURATION, "conv2d systems are not supported by this build yet");
-  if (s->kind != LMG_DENSE && s->kind != LMG_DENSE_ADJOINT)
+  if (s->kind < LMG_DENSE || s->kind > LMG_CONV_ADJOINT)
     return fail(LMG_ERR_CONFIGURATION, "unknown system kind");
+  if (is_conv(*s)) {
+    if (s->channels < 1 || s->height < 1 || s->px_width < 1 ||
+        (int64_t)s->channels * s->height * s->px_width != s->width)
+      return fail(LMG_ERR_DIMENSION, "conv2d geometry does not match the state width");
+  }
   if (s->act < 0 || s->act > 2) return fail(LMG_ERR_CONFIGURATION, "unknown activation");
   if (!s->W) return fail(LMG_ERR_CONFIGURATION, "null weights");
   if (is_adjoint(*s) && !s->D) return fail(LMG_ERR_CONFIGURATION, "adjoint system without D");
@@ -435,6 +514,20 @@ int family(const lmg_system& S, int B, int epi, const Fam& f, cudaStream_t st) {
   a.out2 = f.out2; a.out2_ts = f.out2_ts;
   a.ldc = q;
   a.part = f.part; a.part_slot0 = f.slot0; a.part_ld = B;
+  if (is_conv(S)) {
+    const ConvGeom g = geom_of(S);
+    a.M = B * g.HWp; a.N = g.C; a.K = 9 * g.Cp;
+    if (is_adjoint(S)) {
+      a.act = LMG_ACT_IDENTITY;
+      a.bias = nullptr;
+      a.Ds = S.D + (int64_t)f.blk0 * S.d_stride; a.Ds_ts = (int64_t)f.blk_step * S.d_stride;
+      return launch_conv<CV_ADJ>(a, g, st);
+    }
+    a.act = S.act;
+    a.bias = S.b ? S.b + (int64_t)f.blk0 * S.b_stride : nullptr;
+    a.bias_ts = (int64_t)f.blk_step * S.b_stride;
+    return launch_conv<CV_FWD>(a, g, st);
+  }
   if (is_adjoint(S)) {
     a.act = LMG_ACT_IDENTITY;
     a.bias = nullptr;
@@ -635,7 +728,7 @@ int local_residual_post(const lmg_system& S, int B, int c, const double* U, cons
   const int q = S.width;
   const int64_t BQ = (int64_t)B * q;
   const int nb = S.num_layers / c;
-  const int nt = n_tiles(q);
+  const int nt = row_slots(S);
   double* fpart = work;
   double* cpart = work + (size_t)nb * nt * B;
   TRY(launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
@@ -664,7 +757,7 @@ int local_residual_full_a(const lmg_system& S, int B, const double* U, const dou
   f.x = U; f.x_ts = BQ;
   f.s = src_fam(src, mode, BQ, 1); f.s_ts = BQ;
   f.y = U + BQ; f.y_ts = BQ;
-  f.part = work; f.slot0 = n_tiles(S.width);  // row j's tiles at slot j*nt
+  f.part = work; f.slot0 = row_slots(S);  // row j's tiles at slot j*nt
   TRY(family(S, B, E_RESID, f, st));
   if (has_next && adv_out) {
     Fam g;
@@ -685,7 +778,7 @@ int local_residual_full_b(const lmg_system& S, int B, int c, const double* U, co
   const int64_t BQ = (int64_t)B * q;
   const int L = S.num_layers;
   const int nb = L / c;
-  const int nt = n_tiles(q);
+  const int nt = row_slots(S);
   double* rpart = work;
   double* r0part = work + (size_t)L * nt * B;
   double* tmp = r0part + 2 * (size_t)B;  // one (B, q) row: f[0] + adv_in
@@ -721,7 +814,7 @@ int residual_full(const lmg_system& S, int B, const double* U, const double* src
   f.out = R ? R + BQ : nullptr; f.out_ts = BQ;
   f.part = part; f.slot0 = 1;
   TRY(family(S, B, E_RESID, f, st));
-  *nslots = 1 + (int64_t)(n - 1) * n_tiles(q);
+  *nslots = 1 + (int64_t)(n - 1) * row_slots(S);
   return LMG_OK;
 }
 
@@ -1089,6 +1182,25 @@ int lmg_param_grads(const lmg_system* fine, int B, const double* states, const d
   const int N = fine->num_layers, q = fine->width;
   const int64_t BQ = (int64_t)B * q;
   cudaStream_t st = S_(stream);
+  if (is_conv(*fine)) {
+    // gW[tap][ci][co] = h*scale*sum_{b,pix} (lam*D)[b][co][pix] u[b][ci][pix + shift(tap)]
+    const ConvGeom g = geom_of(*fine);
+    StepArgs a{};
+    a.M = 9 * g.Cp; a.N = g.C; a.K = B * g.HWp; a.ntasks = N;
+    a.epi = E_PGRAD; a.act = LMG_ACT_IDENTITY; a.h = fine->step; a.lr = lr; a.scale = scale;
+    a.A = states; a.A_ts = BQ;
+    a.Bm = lam + (int64_t)(N - 1) * BQ; a.B_ts = -BQ;  // lambda^{n+1} = lam[N-1-n]
+    a.Ds = D; a.Ds_ts = BQ;
+    a.x = fine->W; a.x_ts = fine->w_stride;
+    a.out = const_cast<double*>(fine->W); a.out_ts = fine->w_stride;
+    a.out2 = gW; a.out2_ts = 9LL * g.C * g.C;
+    TRY(launch_conv<CV_PGRAD>(a, g, st));
+    return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
+      k_conv_bias_grads<<<dim3(g.C, N), 256, 0, st>>>(lam + (int64_t)(N - 1) * BQ, -BQ, D, B, g.C,
+                                                     g.HW, fine->step, scale, lr, gb,
+                                                     const_cast<double*>(fine->b), fine->b_stride);
+    });
+  }
   StepArgs a{};
   a.M = q; a.N = q; a.K = B; a.ntasks = N;
   a.epi = E_PGRAD; a.act = LMG_ACT_IDENTITY; a.h = fine->step; a.lr = lr; a.scale = scale;
@@ -1104,6 +1216,49 @@ int lmg_param_grads(const lmg_system* fine, int B, const double* states, const d
   TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_bias_grads<<<(int)((tot + 255) / 256), 256, 0, st>>>(lam + (int64_t)(N - 1) * BQ, -BQ, D, N, B, q,
                                                          fine->step, scale, lr, gb,
                                                          const_cast<double*>(fine->b), fine->b_stride); }));
+  return LMG_OK;
+}
+
+int lmg_apply_block(const lmg_system* sys, int B, int j, const double* X, double* Y, void* stream) {
+  TRY(check_sys(sys, B));
+  if (is_adjoint(*sys)) return fail(LMG_ERR_CONFIGURATION, "apply_block needs a forward system");
+  if (j < 0 || j >= sys->num_layers) return fail(LMG_ERR_DIMENSION, "block index out of range");
+  Fam f;
+  f.ntasks = 1; f.blk0 = j;
+  f.x = X; f.out = Y;
+  return family(*sys, B, E_APPLY, f, S_(stream));
+}
+
+int lmg_vjp_block(const lmg_system* sys, int B, int j, const double* X, const double* G, double* gX,
+                  double* gW, double* gb, double* work, void* stream) {
+  TRY(check_sys(sys, B));
+  if (is_adjoint(*sys)) return fail(LMG_ERR_CONFIGURATION, "vjp_block needs a forward system");
+  if (j < 0 || j >= sys->num_layers) return fail(LMG_ERR_DIMENSION, "block index out of range");
+  cudaStream_t st = S_(stream);
+  Fam f;  // work = act'(pre(X))
+  f.ntasks = 1; f.blk0 = j;
+  f.x = X; f.out = work;
+  TRY(family(*sys, B, E_DERIV, f, st));
+  lmg_system one = *sys;
+  one.num_layers = 1;
+  one.W = sys->W + (int64_t)j * sys->w_stride;
+  one.b = sys->b ? sys->b + (int64_t)j * sys->b_stride : nullptr;
+  one.w_stride = one.b_stride = 0;
+  if (gX) {  // gX = J^T (G * act'): the adjoint block on its own
+    lmg_system adj = one;
+    adj.kind = is_conv(*sys) ? LMG_CONV_ADJOINT : LMG_DENSE_ADJOINT;
+    adj.D = work;
+    adj.d_stride = 0;
+    adj.b = nullptr;
+    Fam g;
+    g.ntasks = 1; g.blk0 = 0;
+    g.x = G; g.out = gX;
+    TRY(family(adj, B, E_APPLY, g, st));
+  }
+  if (gW || gb) {
+    one.step = 1.0;
+    TRY(lmg_param_grads(&one, B, X, G, work, 1.0, 0.0, gW, gb, stream));
+  }
   return LMG_OK;
 }
 

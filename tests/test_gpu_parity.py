@@ -21,6 +21,7 @@ import paper_2007_07336_b200 as P  # noqa: E402
 from paper_2007_07336_b200 import _lib  # noqa: E402
 
 DENSE_CASES = [c for c in SOLVE_CASES if not c.startswith("conv")]
+CONV_CASES = [c for c in SOLVE_CASES if c.startswith("conv")]
 
 
 def dev(a):
@@ -30,7 +31,11 @@ def dev(a):
 def gpu_net(g):
     """Our ResidualNetwork from a golden case's parameters."""
     act = str(g["activation"])
-    blocks = [P.dense_params(g["W"][i], g["b"][i], act) for i in range(len(g["W"]))]
+    if str(g["kind"]) == "conv2d":
+        blocks = [P.conv2d_params(g["Wc"][i], g["b"][i], act, int(g["height"]), int(g["width"]))
+                  for i in range(len(g["Wc"]))]
+    else:
+        blocks = [P.dense_params(g["W"][i], g["b"][i], act) for i in range(len(g["W"]))]
     return P.ResidualNetwork(P.dense_params(g["Wo"], g["bo"], str(g["open_act"])), blocks,
                              P.dense_params(g["Wr"], g["br"], str(g["read_act"])), float(g["step"]))
 
@@ -58,7 +63,7 @@ def test_kat_one_cycle_and_sweeps():
     assert np.max(np.abs(P.propagation_operator(net, g["after"]) - g["propop"])) <= 1e-14
 
 
-@pytest.mark.parametrize("case", DENSE_CASES)
+@pytest.mark.parametrize("case", SOLVE_CASES)
 def test_batched_solve_matches_reference(case):
     g = load(case)
     net = gpu_net(g)
@@ -132,7 +137,7 @@ def test_relaxation_exactness_rows_are_exact_zeros():
     assert np.all(r[~fmask] == 0.0)
 
 
-@pytest.mark.parametrize("case", DENSE_CASES)
+@pytest.mark.parametrize("case", SOLVE_CASES)
 def test_gradients_match_reference(case):
     g = load(case)
     net = gpu_net(g)
@@ -148,7 +153,8 @@ def test_gradients_match_reference(case):
             assert np.max(np.abs(got - want)) <= 1e-10 * scale + 1e-14
 
 
-@pytest.mark.parametrize("case", ["c1_64x32_cf4", "ml3_64x8_cf4", "relu_128x24_cf8_3lvl"])
+@pytest.mark.parametrize("case", ["c1_64x32_cf4", "ml3_64x8_cf4", "relu_128x24_cf8_3lvl",
+                                  "conv_relu_d16_c4x8x8"])
 def test_fas_adjoint_batch_matches_reference_grads(case):
     """The FAS adjoint (no reference implementation) converges to the reference's gradients;
     its residual history matches the oracle's FAS adjoint."""
@@ -163,7 +169,7 @@ def test_fas_adjoint_batch_matches_reference_grads(case):
                    threshold=int(g["threshold"]), tol=1e-12, max_cycles=60, scale=1.0)
     assert all(r.converged)
     gW = r.gW.cpu().numpy()
-    want = g["gW"].sum(axis=0)
+    want = (g["gW"] if "gW" in g else g["gW"]).sum(axis=0)
     assert np.max(np.abs(gW - want)) <= 1e-9 * np.max(np.abs(want))
     np.testing.assert_allclose(r.loss.cpu().numpy(), g["loss"], rtol=1e-12)
     # oracle FAS adjoint history
@@ -233,3 +239,21 @@ def test_larger_solve_against_oracle(N, q, B, c, thr):
     for b in range(B):
         assert cyc[b] == len(hist[b]) - 1
         assert all(band(x, y, N, q) for x, y in zip(h[: cyc[b] + 1, b], hist[b]))
+
+
+def test_conv_transform_and_vjp_against_oracle():
+    """kernels.py:130-136 / 171-188 for single conv blocks (odd geometry, 3 channels, 5x7)."""
+    rng = np.random.default_rng(5)
+    C, H, Wd = 3, 5, 7
+    p = P.conv2d_params(rng.normal(0, 0.3, (3, 3, C, C)), rng.normal(0, 0.1, C), "tanh", H, Wd)
+    lev = fas.ConvLevel(p.weights[None], p.bias[None], "tanh", 1.0, H, Wd)
+    X = rng.normal(size=(4, C * H * Wd))
+    G = rng.normal(size=(4, C * H * Wd))
+    y = P.apply_transform(p, X)
+    assert np.max(np.abs(y - lev.F(0, X))) <= 1e-14
+    gx, gw, gb = P.transform_vjp(p, X, G)
+    D = fas.act_deriv("tanh", lev.pre(0, X))
+    assert np.max(np.abs(gx - lev.vjp_input(0, X, G * D))) <= 1e-13
+    ow, ob = lev.param_grads(0, X, G * D)
+    assert np.max(np.abs(gw - ow)) <= 1e-12 * np.max(np.abs(ow))
+    assert np.max(np.abs(gb - ob)) <= 1e-12 * np.max(np.abs(ob))
