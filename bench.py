@@ -35,6 +35,12 @@ CONFIGS = {
     "c1": dict(depth=64, width=32, batch=64, cf=4, threshold=None, tol=1e-9, max_cycles=50, lr=0.1,
                workload="dense tanh ResNet 64 layers width 32 batch 64, 2-level FAS cf 4 "
                         "forward+adjoint training step to tol 1e-9"),
+    # BASELINE.json configs[2]: conv ResNet (3x3 conv + bias + ReLU, 64 channels, 32x32), 256 layers
+    "c3": dict(kind="conv", depth=256, width=64 * 32 * 32, channels=64, side=32, batch=32, cf=4,
+               threshold=16, tol=1e-9, max_cycles=50, lr=0.1, input_dim=64,
+               workload="conv ResNet 256 layers (3x3 conv+bias+ReLU, 64 ch, 32x32) batch 32, 3-level "
+                        "FAS (cf 4, levels [256,64,16]) forward+adjoint training step to tol 1e-9; "
+                        "dense tanh opening from 64 features"),
     # configs[4]-style HBM-bound point (q=512, B=16, cf 16)
     "c5": dict(depth=1024, width=512, batch=16, cf=16, threshold=4, tol=1e-9, max_cycles=50, lr=0.1,
                workload="dense tanh ResNet 1024 layers width 512 batch 16, 3-level FAS cf 16 "
@@ -86,11 +92,23 @@ def cpu_reference_sample(cfg, fwd_cycles: int, nsamp: int | None = None):
     N, q = cfg["depth"], cfg["width"]
     nsamp = nsamp or min(cfg["batch"], max(4, min(8, os.cpu_count() or 4)))
     key = (N, q)
+    conv = cfg.get("kind") == "conv"
     if key not in _NET_CACHE:
         _NET_CACHE.clear()
-        _NET_CACHE[key] = fas.net_from_arrays(fas.random_network_arrays(N, q, [0, N, q]))
+        if conv:
+            from paper_2007_07336_b200.synthetic import conv_network_arrays
+
+            a = conv_network_arrays(N, cfg["channels"], cfg["side"], [0, N, cfg["channels"]],
+                                    input_dim=cfg["input_dim"])
+            fine = fas.ConvLevel(a["Wc"], a["b"], a["activation"], a["step"], a["side"], a["side"])
+            _NET_CACHE[key] = fas.Net(a["Wo"], a["bo"], "tanh", fine, a["Wr"], a["br"], "identity")
+        else:
+            _NET_CACHE[key] = fas.net_from_arrays(fas.random_network_arrays(N, q, [0, N, q]))
     net = _NET_CACHE[key]
-    X = np.stack([fas.random_sample(q, [0, N, q, b]) for b in range(nsamp)])
+    din = cfg.get("input_dim", q)
+    if conv:
+        nsamp = 1  # one conv sample already is ~20 s of host work
+    X = np.stack([fas.random_sample(din, [0, N, q, b]) for b in range(nsamp)])
     labels = np.arange(nsamp) % 10
     t0 = time.perf_counter()
     src = net.source(X)
@@ -98,7 +116,7 @@ def cpu_reference_sample(cfg, fwd_cycles: int, nsamp: int | None = None):
     U = fas.initial_guess(levels[0], src)
     fas.l2_norms(fas.compute_residual(levels[0], U, src))
     t1 = time.perf_counter()
-    ncyc = 2
+    ncyc = 1 if conv else 2
     for _ in range(ncyc):
         fas.mg_cycle(levels, cfg["cf"], U, src)
     t2 = time.perf_counter()
@@ -124,7 +142,7 @@ def run_reference(args, cfg):
     times, vals = [], []
     info = None
     # the number of forward cycles the solve needs at this config (c2: 36)
-    cyc = {"c2": 36, "c1": 7, "c5": 8}[args.config]
+    cyc = {"c2": 36, "c1": 7, "c5": 8, "c3": 16}[args.config]
     for i in range(args.warmup + args.steps):
         v, info = cpu_reference_sample(cfg, cyc)
         if i >= args.warmup:
@@ -212,8 +230,9 @@ def fp64_peak_tflops(torch, dev):
     return best
 
 
-def load_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+def load_traffic(config):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary
+    (only when that capture was taken on this config)."""
     import glob
 
     cands = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
@@ -223,6 +242,8 @@ def load_traffic():
     try:
         with open(p) as fh:
             d = json.load(fh)
+        if d.get("config") != config:
+            return None, d
         return d.get("dram_bytes_per_launch"), d
     except (OSError, ValueError):
         return None, None
@@ -249,7 +270,9 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=dev)
 
     N, q, B = cfg["depth"], cfg["width"], cfg["batch"]
-    X_host = torch.from_numpy(P.random_batch(q, [0, N, q], B)).pin_memory()
+    conv = cfg.get("kind") == "conv"
+    din = cfg.get("input_dim", q)
+    X_host = torch.from_numpy(P.random_batch(din, [0, N, q], B)).pin_memory()
     lab_host = torch.from_numpy(np.arange(B) % 10).pin_memory()
     X = X_host.to(dev)
     labels = lab_host.to(dev)
@@ -261,7 +284,13 @@ def run_ours(args, cfg):
                                   tol=cfg["tol"], max_cycles=cfg["max_cycles"], adjoint=args.adjoint,
                                   learning_rate=cfg["lr"])
     else:
-        d = P.device_network(N, q, [0, N, q], device=dev)
+        if conv:
+            from paper_2007_07336_b200.synthetic import conv_device_network
+
+            d = conv_device_network(N, cfg["channels"], cfg["side"], [0, N, cfg["channels"]],
+                                    device=dev, input_dim=din)
+        else:
+            d = P.device_network(N, q, [0, N, q], device=dev)
         tr = P.DeviceTrainer(d, coarsening=cfg["cf"], threshold=cfg["threshold"], tol=cfg["tol"],
                              max_cycles=cfg["max_cycles"], adjoint=args.adjoint,
                              learning_rate=cfg["lr"])
@@ -303,6 +332,35 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
 
+    # ---- serial layer-by-layer GPU propagation of the same step (north_star comparison): the
+    # reference's sequential forward + sequential adjoint + gradients + SGD, same kernels
+    serial_ms = None
+    if world == 1:
+        from paper_2007_07336_b200 import _lib as L_
+        from paper_2007_07336_b200.training import _dense_apply, backward
+
+        dn = tr.dnet
+        view = dn._lmg_view()
+        Us = torch.empty((N, B, q), dtype=torch.float64, device=dev)
+
+        def serial_step():
+            f0 = _dense_apply(dn.Wo, dn.bo, dn.open_act, X)
+            L_.call("lmg_sequential_forward", view.desc(), B, f0.data_ptr(), L_.SRC_HEAD,
+                    Us.data_ptr(), L_.stream_handle())
+            backward(dn, Us, X, labels, adjoint="sequential", scale=1.0 / B, lr=cfg["lr"],
+                     want_grads=False)
+
+        serial_step()
+        barrier()
+        s3, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s3.record()
+        for _ in range(args.steps):
+            serial_step()
+        e3.record()
+        barrier()
+        serial_ms = s3.elapsed_time(e3) / args.steps
+        del Us
+
     # ---- e2e: same step through the public API from pinned host buffers, result read back
     barrier()
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -325,7 +383,7 @@ def run_ours(args, cfg):
     gemm_ms = f_ms + a_ms
     gemm_flops = f_flops + a_flops
     achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
-    traffic, prof = load_traffic()
+    traffic, prof = load_traffic(args.config)
     line = dict(
         metric=METRIC,
         value=N * B / (ms * 1e-3),
@@ -355,6 +413,13 @@ def run_ours(args, cfg):
         v, info = cpu_reference_sample(cfg, cycles[-1][0])
         line["cpu_baseline"] = dict(value=v, unit=UNIT, cores=info["cores"], kind="port",
                                     sample=info["sample"])
+    if serial_ms is not None:
+        line["serial_gpu"] = dict(
+            value=N * B / (serial_ms * 1e-3), unit=UNIT, ms_per_step=serial_ms,
+            what="layer-by-layer GPU propagation of the same step with the same kernels: "
+                 "sequential_forward (network.py:111-123) + the reference's sequential adjoint "
+                 "(training.py:216-224) + gradients + SGD",
+            fas_over_serial_time=ms / serial_ms)
     line["clocks"] = clk.summary()
     if rank == 0:
         print(json.dumps(line))

@@ -157,8 +157,10 @@ int lmg_param_grads(const lmg_system* fine, int B, const double* states, const d
  * adv_out after fcf_b.  Single GPU == is_first = 1, has_next = 0.  States are bitwise identical
  * for every partition; norms too, since partials are per block and summed in global block order.
  */
+/* Q (optional, nb rows): propagate(U[kc]) from the previous cycle's lmg_local_residual_post; when
+ * given, the first F-sweep step is a copy instead of a launch (bitwise identical). */
 int lmg_local_fcf_a(const lmg_system* sys, int B, int c, double* U, const double* src,
-                    int src_mode, int is_first, int has_next, void* stream);
+                    int src_mode, int is_first, int has_next, const double* Q, void* stream);
 int lmg_local_fcf_b(const lmg_system* sys, int B, int c, double* U, const double* src,
                     int src_mode, double* P, int has_next, double* adv_out, void* stream);
 int lmg_halo_finish(const double* s0, const double* adv_in, double* out, int64_t len, void* stream);
@@ -170,7 +172,7 @@ int lmg_local_correct(int n_blocks, int B, int q, int c, double* U, const double
 size_t lmg_local_workspace(int L, int B, int q);
 int lmg_local_residual_post(const lmg_system* sys, int B, int c, const double* U,
                             const double* src, int src_mode, const double* P, int is_first,
-                            double* block_part, void* work, void* stream);
+                            double* block_part, void* work, double* Q, void* stream);
 int lmg_local_residual_full_a(const lmg_system* sys, int B, const double* U, const double* src,
                               int src_mode, int has_next, double* adv_out, void* work,
                               void* stream);

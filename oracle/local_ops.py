@@ -56,11 +56,17 @@ class NumpyOps:
 
         return row
 
-    def fcf_a(self, lv, U, S, smode, is_first, has_next):
+    def fcf_a(self, lv, U, S, smode, is_first, has_next, Q=None):
         lev, u, c, nb = lv.desc(), _a(U), lv.c, lv.nb
         h, sr = lev.step, self._src(S, smode)
         K1 = nb - 1 + int(has_next)
-        for s in range(c - 1):
+        s0 = 0
+        if Q is not None:
+            q = _a(Q)
+            for k in range(K1):
+                u[k * c + 1] = q[k]
+            s0 = 1
+        for s in range(s0, c - 1):
             for k in range(K1):
                 j = k * c + s + 1
                 u[j] = sr(j) + (u[j - 1] + h * lev.F(j - 1, u[j - 1]))
@@ -112,14 +118,18 @@ class NumpyOps:
         for k in range(lv.nb):
             u[k * c] = u[k * c] + (v[k] - u[k * c])
 
-    def residual_post(self, lv, U, S, smode, P, is_first, block_part, work):
+    def residual_post(self, lv, U, S, smode, P, is_first, block_part, work, Q=None):
         lev, u, c, nb = lv.desc(), _a(U), lv.c, lv.nb
         h, sr, p = lev.step, self._src(S, smode), _a(P)
         bp = _a(block_part)
+        qq = _a(Q)
         for k in range(nb):
             rc = (sr(0) - u[0]) if (k == 0 and is_first) else (p[k] - u[k * c])
             j = k * c + 1
-            rf = (sr(j) + (u[j - 1] + h * lev.F(j - 1, u[j - 1]))) - u[j]
+            prop = sr(j) + (u[j - 1] + h * lev.F(j - 1, u[j - 1]))
+            if qq is not None:
+                qq[k] = prop
+            rf = prop - u[j]
             bp[k] = (np.asarray(rc) ** 2).sum(axis=-1) + (rf ** 2).sum(axis=-1)
 
     def residual_full_a(self, lv, U, S, smode, has_next, adv_out, work):

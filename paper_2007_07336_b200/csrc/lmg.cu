@@ -619,11 +619,18 @@ int c_relax(const lmg_system& S, int B, int c, double* U, const double* src, int
 // is consumed at s = 0, before the C step overwrites it at s = c-1; without has_next the last
 // block's first sweep is dead in the reference (overwritten, never read) and is skipped.
 int local_fcf_a(const lmg_system& S, int B, int c, double* U, const double* src, int mode,
-                bool is_first, bool has_next, cudaStream_t st) {
+                bool is_first, bool has_next, const double* Q, cudaStream_t st) {
   const int64_t BQ = (int64_t)B * S.width;
   const int nb = S.num_layers / c;
   const int K1 = nb - 1 + (has_next ? 1 : 0);
-  for (int s = 0; s + 1 < c; ++s) {
+  int s0 = 0;
+  if (Q && c > 1) {
+    // rows kc+1 = propagate(U[kc]) were produced by the previous cycle's residual (Q) from the
+    // same, unchanged U[kc]: copy instead of recomputing (bitwise identical)
+    TRY(copy_rows(U + BQ, c * BQ, Q, BQ, K1, BQ, st));
+    s0 = 1;
+  }
+  for (int s = s0; s + 1 < c; ++s) {
     Fam f;
     f.ntasks = K1; f.blk0 = s; f.blk_step = c;
     f.x = U + (int64_t)s * BQ; f.x_ts = c * BQ;
@@ -674,7 +681,7 @@ int local_fcf_b(const lmg_system& S, int B, int c, double* U, const double* src,
 // plain FCF on a whole level (multigrid.py:160-172)
 int fcf(const lmg_system& S, int B, int c, double* U, const double* src, int mode, double* P,
         cudaStream_t st) {
-  TRY(local_fcf_a(S, B, c, U, src, mode, true, false, st));
+  TRY(local_fcf_a(S, B, c, U, src, mode, true, false, nullptr, st));
   return local_fcf_b(S, B, c, U, src, mode, P, false, nullptr, st);
 }
 
@@ -724,7 +731,7 @@ size_t local_part_doubles(int L, int B, int q) {
 // the step GEMM, everything else exactly zero.  Writes canonical per-block partials nb x B.
 int local_residual_post(const lmg_system& S, int B, int c, const double* U, const double* src,
                         int mode, const double* P, bool is_first, double* block_part, double* work,
-                        cudaStream_t st) {
+                        double* Q, cudaStream_t st) {
   const int q = S.width;
   const int64_t BQ = (int64_t)B * q;
   const int nb = S.num_layers / c;
@@ -739,6 +746,7 @@ int local_residual_post(const lmg_system& S, int B, int c, const double* U, cons
   f.x = U; f.x_ts = c * BQ;
   f.s = src_fam(src, mode, BQ, 1); f.s_ts = c * BQ;
   f.y = U + BQ; f.y_ts = c * BQ;
+  f.out2 = Q; f.out2_ts = BQ;
   f.part = fpart; f.slot0 = 0;
   TRY(family(S, B, E_RESID, f, st));
   return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
@@ -844,6 +852,7 @@ struct Workspace {
   std::vector<double*> P, SH, V;  // per relaxed level l: P[l]; per coarse level l+1: SH, V
   double* part = nullptr;         // residual partial-sum scratch
   double* block_part = nullptr;   // canonical per-block partials (N/c x B)
+  double* Q = nullptr;            // finest level: propagate(U[kc]) rows from the last residual
   double* norms = nullptr;
   size_t bytes = 0;
 };
@@ -871,6 +880,7 @@ int layout_ws(const lmg_system& fine, int nlevels, int c, int B, char* base, Wor
   }
   ws->part = take(local_part_doubles(fine.num_layers, B, fine.width));
   ws->block_part = take((size_t)(fine.num_layers / c + 1) * B);
+  ws->Q = take((size_t)(fine.num_layers / c + 1) * BQ);
   ws->norms = take((size_t)B);
   ws->bytes = off;
   return LMG_OK;
@@ -894,7 +904,8 @@ int full_norms(const lmg_system& S, int B, int c, const double* U, const double*
 // multigrid.py:175-228 on one GPU.  `want_norm` only at the finest level: the recursive call's
 // return value is discarded by the reference (multigrid.py:218-226).
 int cycle(const lmg_system& S, int nlevels, int l, int c, int B, double* U, const double* src,
-          int mode, const Workspace& ws, bool want_norm, double* norms, cudaStream_t st) {
+          int mode, const Workspace& ws, bool want_norm, double* norms, cudaStream_t st,
+          bool q_valid = false) {
   if (l == nlevels - 1) {  // single-level hierarchy: exact solve
     TRY(seq_forward(S, B, src, mode, U, st));
     if (want_norm) TRY(full_norms(S, B, c, U, src, mode, ws, norms, st));
@@ -902,7 +913,7 @@ int cycle(const lmg_system& S, int nlevels, int l, int c, int B, double* U, cons
   }
   const int nb = S.num_layers / c;
   double* P = ws.P[l];
-  TRY(local_fcf_a(S, B, c, U, src, mode, true, false, st));
+  TRY(local_fcf_a(S, B, c, U, src, mode, true, false, (l == 0 && q_valid) ? ws.Q : nullptr, st));
   TRY(local_fcf_b(S, B, c, U, src, mode, P, false, nullptr, st));
   const lmg_system Sc = coarsen(S, c);
   const bool coarsest = (l + 1 == nlevels - 1);
@@ -915,7 +926,8 @@ int cycle(const lmg_system& S, int nlevels, int l, int c, int B, double* U, cons
     TRY(cycle(Sc, nlevels, l + 1, c, B, V, SH, LMG_SRC_DENSE, ws, false, nullptr, st));
   TRY(local_correct(nb, B, S.width, c, U, V, st));
   if (want_norm) {
-    TRY(local_residual_post(S, B, c, U, src, mode, P, true, ws.block_part, ws.part, st));
+    TRY(local_residual_post(S, B, c, U, src, mode, P, true, ws.block_part, ws.part,
+                            l == 0 ? ws.Q : nullptr, st));
     TRY(norms_from_blocks(ws.block_part, nb, B, norms, st));
   }
   return LMG_OK;
@@ -1136,7 +1148,7 @@ int lmg_solve(const lmg_system* fine, int nlevels, int c, int B, double* states,
 
   int cyc = 0;
   while (ndone < B && cyc < max_cycles) {
-    TRY(cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st));
+    TRY(cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, cyc > 0));
     ++cyc;
     CUDA_TRY(cudaMemcpyAsync(nrm.data(), ws.norms, B * sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
@@ -1265,10 +1277,10 @@ int lmg_vjp_block(const lmg_system* sys, int B, int j, const double* X, const do
 // ---- partition-aware level operations (include/lmg.h "layer-partitioned" section) ----------
 
 int lmg_local_fcf_a(const lmg_system* sys, int B, int c, double* U, const double* src,
-                    int src_mode, int is_first, int has_next, void* stream) {
+                    int src_mode, int is_first, int has_next, const double* Q, void* stream) {
   TRY(check_sys(sys, B));
   TRY(check_levels(*sys, 2, c));
-  return local_fcf_a(*sys, B, c, U, src, src_mode, is_first != 0, has_next != 0, S_(stream));
+  return local_fcf_a(*sys, B, c, U, src, src_mode, is_first != 0, has_next != 0, Q, S_(stream));
 }
 
 int lmg_local_fcf_b(const lmg_system* sys, int B, int c, double* U, const double* src,
@@ -1305,11 +1317,11 @@ size_t lmg_local_workspace(int L, int B, int q) {
 
 int lmg_local_residual_post(const lmg_system* sys, int B, int c, const double* U,
                             const double* src, int src_mode, const double* P, int is_first,
-                            double* block_part, void* work, void* stream) {
+                            double* block_part, void* work, double* Q, void* stream) {
   TRY(check_sys(sys, B));
   TRY(check_levels(*sys, 2, c));
   return local_residual_post(*sys, B, c, U, src, src_mode, P, is_first != 0, block_part,
-                             reinterpret_cast<double*>(work), S_(stream));
+                             reinterpret_cast<double*>(work), Q, S_(stream));
 }
 
 int lmg_local_residual_full_a(const lmg_system* sys, int B, const double* U, const double* src,

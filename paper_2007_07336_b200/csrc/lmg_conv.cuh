@@ -254,8 +254,10 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
         } else if (epi == E_PROP) {
           O[idx] = __dadd_rn(S ? S[idx] : 0.0, adv);
         } else if (epi == E_RESID) {
-          const double r = __dadd_rn(__dadd_rn(S ? S[idx] : 0.0, adv), -Y[idx]);
+          const double prop = __dadd_rn(S ? S[idx] : 0.0, adv);
+          const double r = __dadd_rn(prop, -Y[idx]);
           if (O) O[idx] = r;
+          if (O2) O2[idx] = prop;
           sq = fma(r, r, sq);
         } else if (epi == E_COARSE) {
           const double yv = Y[idx];

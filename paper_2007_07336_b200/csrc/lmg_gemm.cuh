@@ -33,7 +33,7 @@ namespace lmg {
 
 enum Epi {
   E_PROP = 0,      // out = s + (x + h*act(pre))                       network.py:100
-  E_RESID = 1,     // r = (s + (x + h*act(pre))) - y; out=r; sum r^2   multigrid.py:124-127
+  E_RESID = 1,     // r = (s + (x + h*act(pre))) - y; out=r; out2=s+(..); sum r^2  multigrid.py:124-127
   E_COARSE = 2,    // out = (y - (x + h*act(pre))) + (p - y); out2 = y multigrid.py:142, network.py:138
   E_COARSE_R = 3,  // out = (y - (x + h*act(pre))) + p                 multigrid.py:142
   E_PROPOP = 4,    // out = y - (x + h*act(pre))                       network.py:138
@@ -252,8 +252,10 @@ __device__ __forceinline__ void epilogue(const StepArgs& a, const EpiPtrs& q, do
         } else if (EPI == E_PROP) {
           q.O[idx] = __dadd_rn(q.S ? q.S[idx] : 0.0, adv);
         } else if (EPI == E_RESID) {
-          double r = __dadd_rn(__dadd_rn(q.S ? q.S[idx] : 0.0, adv), -q.Y[idx]);
+          const double prop = __dadd_rn(q.S ? q.S[idx] : 0.0, adv);
+          double r = __dadd_rn(prop, -q.Y[idx]);
           if (q.O) q.O[idx] = r;
+          if (q.O2) q.O2[idx] = prop;  // the propagated row, reused by the next F sweep
           rowsq[i] = fma(r, r, rowsq[i]);
         } else if (EPI == E_COARSE) {
           const double yv = q.Y[idx];

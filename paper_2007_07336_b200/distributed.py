@@ -44,9 +44,9 @@ class CudaOps:
     def _p(t):
         return None if t is None else t.data_ptr()
 
-    def fcf_a(self, lv, U, S, smode, is_first, has_next):
+    def fcf_a(self, lv, U, S, smode, is_first, has_next, Q=None):
         _lib.call("lmg_local_fcf_a", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
-                  int(is_first), int(has_next), self._st())
+                  int(is_first), int(has_next), self._p(Q), self._st())
 
     def fcf_b(self, lv, U, S, smode, P, has_next, adv_out):
         _lib.call("lmg_local_fcf_b", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
@@ -64,9 +64,10 @@ class CudaOps:
     def correct(self, lv, U, V):
         _lib.call("lmg_local_correct", lv.nb, lv.B, lv.q, lv.c, U.data_ptr(), V.data_ptr(), self._st())
 
-    def residual_post(self, lv, U, S, smode, P, is_first, block_part, work):
+    def residual_post(self, lv, U, S, smode, P, is_first, block_part, work, Q=None):
         _lib.call("lmg_local_residual_post", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
-                  P.data_ptr(), int(is_first), block_part.data_ptr(), work.data_ptr(), self._st())
+                  P.data_ptr(), int(is_first), block_part.data_ptr(), work.data_ptr(), self._p(Q),
+                  self._st())
 
     def residual_full_a(self, lv, U, S, smode, has_next, adv_out, work):
         _lib.call("lmg_local_residual_full_a", lv.desc(), lv.B, U.data_ptr(), self._p(S), smode,
@@ -161,6 +162,8 @@ class DistSolver:
             self.U.append(z(L + 1, B, q) if l > 0 else None)   # level 0 states are the caller's
             self.S.append(z(L + 1, B, q) if l > 0 else None)   # coarse sources, zero row L
             self.P.append(z(lev.nb + 2, B, q) if l < nlevels - 1 else None)  # + [P_out, adv_out]
+        self.Q = z(lv.nb + 1, B, q)  # finest level: propagated rows kc+1 of the last residual
+        self.q_valid = False
         self.recv1 = z(1, B, q)
         self.recv2 = z(2, B, q)
         self.work = z(ops.work_doubles(lv.L + 1, B, q))
@@ -242,7 +245,8 @@ class DistSolver:
         ops = self.ops
         nb, c = lev.nb, self.c
         P = self.P[l]
-        ops.fcf_a(lev, U, S, smode, self.is_first, self.has_next)
+        ops.fcf_a(lev, U, S, smode, self.is_first, self.has_next,
+                  self.Q if (l == 0 and self.q_valid) else None)
         self._exchange(U[lev.L : lev.L + 1] if self.has_next else None, self.recv1)
         if not self.is_first:
             ops.halo_finish(None if S is None else S[0], self.recv1[0], U[0])
@@ -261,7 +265,10 @@ class DistSolver:
             self.cycle(l + 1, Vn, SHn, _lib.SRC_DENSE, False)
         ops.correct(lev, U, Vn)
         if want_norm:
-            ops.residual_post(lev, U, S, smode, P, self.is_first, self.block_part, self.work)
+            ops.residual_post(lev, U, S, smode, P, self.is_first, self.block_part, self.work,
+                              self.Q if l == 0 else None)
+            if l == 0:
+                self.q_valid = True
             return self._gather_norms(lev, self.block_part)
         return None
 
@@ -279,6 +286,7 @@ class DistSolver:
                 # initial_guess tiles source row 0 of the FIRST rank (multigrid.py:257-260)
                 pass
             self._broadcast_head(U0, S0, smode)
+        self.q_valid = False
         nrm = self.initial_norms(U0, S0, smode).cpu().numpy()
         hist = np.full((max_cycles + 1, B), np.nan)
         hist[0] = nrm

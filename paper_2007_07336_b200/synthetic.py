@@ -117,3 +117,37 @@ def device_network(depth: int, width: int, seed, *, horizon: float = DEFAULT_HOR
 
 def _check_math():  # pragma: no cover - documentation of the corner handled above
     assert math.copysign(1.0, 0 + -0.0) == 1.0
+
+
+# --- conv2d networks (BASELINE configs[2]) -------------------------------------------------------
+#
+# The reference has no conv generator; this follows the survey's recipe:
+# rng = default_rng(seed); per block (in order) weights N(0, 1/sqrt(9 C)) of shape (3, 3, C, C)
+# then bias N(0, 0.05); step horizon/depth; then a dense tanh opening from `input_dim` features
+# (N(0, 1/sqrt(input_dim)), bias N(0, 0.05)) and a dense identity readout (N(0, 1/sqrt(q))).
+
+
+def conv_network_arrays(depth: int, channels: int, side: int, seed, *, horizon: float = DEFAULT_HORIZON,
+                        activation: str = "relu", input_dim: int = 64, num_classes: int = NUM_CLASSES):
+    rng = np.random.default_rng(seed)
+    C = channels
+    Wc = np.empty((depth, 3, 3, C, C))
+    b = np.empty((depth, C))
+    for n in range(depth):
+        Wc[n] = rng.normal(0.0, 1.0 / np.sqrt(9 * C), (3, 3, C, C))
+        b[n] = rng.normal(0.0, 0.05, C)
+    q = C * side * side
+    Wo = rng.normal(0.0, 1.0 / np.sqrt(input_dim), (q, input_dim))
+    bo = rng.normal(0.0, 0.05, q)
+    Wr = rng.normal(0.0, 1.0 / np.sqrt(q), (num_classes, q))
+    return dict(Wc=Wc, b=b, Wo=Wo, bo=bo, Wr=Wr, br=np.zeros(num_classes), step=horizon / depth,
+                activation=activation, side=side, channels=C)
+
+
+def conv_device_network(depth: int, channels: int, side: int, seed, *, device=None, **kw) -> DeviceNet:
+    t = require_cuda()
+    dev = t.device("cuda") if device is None else t.device(device)
+    a = conv_network_arrays(depth, channels, side, seed, **kw)
+    d = lambda x: t.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+    stack = DeviceStack(d(a["Wc"]), d(a["b"]), a["activation"], "conv2d", (channels, side, side))
+    return DeviceNet(stack, a["step"], d(a["Wo"]), d(a["bo"]), "tanh", d(a["Wr"]), d(a["br"]), "identity")
