@@ -60,6 +60,8 @@ def parse():
     p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     p.add_argument("--adjoint", default="fas", choices=["fas", "sequential"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--split", type=int, default=None,
+                   help="batch slices on concurrent streams (default: 2 when B >= 64)")
     return p.parse_args()
 
 
@@ -291,9 +293,10 @@ def run_ours(args, cfg):
                                     device=dev, input_dim=din)
         else:
             d = P.device_network(N, q, [0, N, q], device=dev)
+        split = args.split if args.split is not None else 1
         tr = P.DeviceTrainer(d, coarsening=cfg["cf"], threshold=cfg["threshold"], tol=cfg["tol"],
                              max_cycles=cfg["max_cycles"], adjoint=args.adjoint,
-                             learning_rate=cfg["lr"])
+                             learning_rate=cfg["lr"], split=split)
     peak = fp64_peak_tflops(torch, dev)
 
     def barrier():
@@ -392,7 +395,8 @@ def run_ours(args, cfg):
         dtype="f64", data="synthetic (reference seeded generators: random_network / random_sample)",
         config=dict(workload=cfg["workload"], depth=N, width=q, batch=B, coarsening=cfg["cf"],
                     threshold=cfg["threshold"], tol=cfg["tol"], adjoint=args.adjoint,
-                    parallelism=f"layer-partitioned x{world}" if world > 1 else "single GPU",
+                    parallelism=(f"layer-partitioned x{world}" if world > 1 else
+                                 f"single GPU, {getattr(tr, 'split', 1)} batch slice(s) on concurrent streams"),
                     l2="inputs larger than L2 (theta 2 GiB, states 1 GiB), no flush",
                     cycles_per_step=cycles),
         e2e=dict(value=N * B / (e2e_ms * 1e-3), unit=UNIT,

@@ -146,6 +146,12 @@ int lmg_act_deriv(const lmg_system* fine, int B, const double* states, double* D
 int lmg_param_grads(const lmg_system* fine, int B, const double* states, const double* lam,
                     const double* D, double scale, double lr, double* gW, double* gb,
                     void* stream);
+/* Same, for one slice of a batch: with accumulate != 0 the slice's gradients are ADDED to gW / gb
+ * (which then must be given), and the SGD step (lr != 0) uses the accumulated gradient -- the
+ * reference's Gradients.accumulate + sgd_update over batch slices (training.py:174-177,287-288). */
+int lmg_param_grads_ex(const lmg_system* fine, int B, const double* states, const double* lam,
+                       const double* D, double scale, double lr, double* gW, double* gb,
+                       int accumulate, void* stream);
 
 /* ---- layer-partitioned level operations -------------------------------------------
  * A rank owns L = nb*c consecutive states of a level (nb whole blocks of the reference's

@@ -75,6 +75,7 @@ SIGNATURES = {
                        c_int32_p, _P, ctypes.c_size_t, _P]),
     "lmg_act_deriv": (_I, [_SYS, _I, _P, _P, _P]),
     "lmg_param_grads": (_I, [_SYS, _I, _P, _P, _P, _D, _D, _P, _P, _P]),
+    "lmg_param_grads_ex": (_I, [_SYS, _I, _P, _P, _P, _D, _D, _P, _P, _I, _P]),
     "lmg_local_fcf_a": (_I, [_SYS, _I, _I, _P, _P, _I, _I, _I, _P, _P]),
     "lmg_local_fcf_b": (_I, [_SYS, _I, _I, _P, _P, _I, _P, _I, _P, _P]),
     "lmg_halo_finish": (_I, [_P, _P, _P, ctypes.c_int64, _P]),

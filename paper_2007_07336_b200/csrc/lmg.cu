@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -134,7 +135,7 @@ __global__ void k_reduce_norms(const double* __restrict__ part, int64_t nslots, 
 __global__ void k_bias_grads(const double* __restrict__ lam_top, int64_t lam_ts,
                              const double* __restrict__ D, int N, int B, int q, double h,
                              double scale, double lr, double* __restrict__ gb,
-                             double* __restrict__ bias, int64_t b_stride) {
+                             double* __restrict__ bias, int64_t b_stride, int accum = 0) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)N * q) return;
   int n = (int)(e / q), i = (int)(e - (int64_t)n * q);
@@ -143,6 +144,7 @@ __global__ void k_bias_grads(const double* __restrict__ lam_top, int64_t lam_ts,
   double s = 0.0;
   for (int b = 0; b < B; ++b) s += __dmul_rn(L[(int64_t)b * q + i], Dn[(int64_t)b * q + i]);
   double g = __dmul_rn(__dmul_rn(s, h), scale);
+  if (accum && gb) g = __dadd_rn(gb[e], g);
   if (gb) gb[e] = g;
   if (lr != 0.0 && bias) {
     double* bp = bias + (int64_t)n * b_stride + i;
@@ -233,7 +235,7 @@ __global__ void k_combine_full(const double* __restrict__ rpart, const double* _
 __global__ void k_conv_bias_grads(const double* __restrict__ lam_top, int64_t lam_ts,
                                   const double* __restrict__ D, int B, int C, int HW, double h,
                                   double scale, double lr, double* __restrict__ gb,
-                                  double* __restrict__ bias, int64_t b_stride) {
+                                  double* __restrict__ bias, int64_t b_stride, int accum = 0) {
   __shared__ double sh[256];
   const int co = blockIdx.x, n = blockIdx.y;
   const int64_t q = (int64_t)C * HW;
@@ -252,7 +254,8 @@ __global__ void k_conv_bias_grads(const double* __restrict__ lam_top, int64_t la
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    const double g = __dmul_rn(__dmul_rn(sh[0], h), scale);
+    double g = __dmul_rn(__dmul_rn(sh[0], h), scale);
+    if (accum && gb) g = __dadd_rn(gb[(int64_t)n * C + co], g);
     if (gb) gb[(int64_t)n * C + co] = g;
     if (lr != 0.0 && bias) {
       double* bp = bias + (int64_t)n * b_stride + co;
@@ -282,6 +285,7 @@ struct Rec {
 std::atomic<unsigned long long> g_launches{0};
 bool g_timing = false;
 std::vector<Rec> g_recs;
+std::mutex g_rec_mu;  // several host threads (one per stream) may launch concurrently
 std::vector<cudaEvent_t> g_pool;
 size_t g_pool_used = 0;
 
@@ -297,15 +301,18 @@ cudaEvent_t pool_event() {
 template <class F>
 int launch(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
   Rec r{cls, flops, bytes, nullptr, nullptr};
-  if (g_timing) {
+  const bool timing = g_timing;
+  if (timing) {
+    std::lock_guard<std::mutex> lk(g_rec_mu);
     r.a = pool_event();
-    cudaEventRecord(r.a, st);
+    r.b = pool_event();
   }
+  if (timing) cudaEventRecord(r.a, st);
   f();
   CUDA_TRY(cudaGetLastError());
-  if (g_timing) {
-    r.b = pool_event();
+  if (timing) {
     cudaEventRecord(r.b, st);
+    std::lock_guard<std::mutex> lk(g_rec_mu);
     g_recs.push_back(r);
   }
   ++g_launches;
@@ -335,16 +342,14 @@ enum Layout { L_FWD = 0, L_ADJ = 1, L_PG = 2 };
 using TSmall = Tile<32, 32, 16, 2, 2, 4>;  // 4 warps of 16x16, ~5 CTAs/SM
 using TWide = Tile<32, 64, 16, 2, 4, 4>;   // 8 warps of 16x16
 
-template <class T, bool AK, bool BKM, bool ASC, int VEC>
+template <class T, bool AK, bool BKM, bool ASC, int VEC, bool FULL = false>
 int launch_cfg(const StepArgs& a, cudaStream_t st) {
   using C = GemmCfg<T, AK, BKM, ASC>;
   constexpr int BM = C::BM, BN = C::BN;
-  auto kern = step_gemm<T, AK, BKM, ASC, VEC>;
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    attr = true;
-  }
+  auto kern = step_gemm<T, AK, BKM, ASC, VEC, FULL>;
+  static const cudaError_t attr =  // thread-safe one-time init
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (attr != cudaSuccess) return fail(LMG_ERR_CUDA, cudaGetErrorString(attr));
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, a.ntasks);
   const int cls = AK ? (BKM ? CLS_GEMM_FWD : CLS_GEMM_ADJ) : CLS_GEMM_PG;
   // algorithmic work: 2MNK per task + ~5 epilogue flops per output (2q^2+5q per F)
@@ -387,7 +392,14 @@ int choose_tile(const StepArgs& a) {
 template <bool AK, bool BKM, bool ASC>
 int launch_layout(const StepArgs& a, bool v2, cudaStream_t st) {
   if (!v2) return launch_cfg<TSmall, AK, BKM, ASC, 1>(a, st);
-  if (choose_tile<AK, BKM, ASC>(a) == SEL_WIDE) return launch_cfg<TWide, AK, BKM, ASC, 2>(a, st);
+  auto full = [&](int BM, int BN, int BK) {
+    return a.M % BM == 0 && a.N % BN == 0 && a.K % BK == 0 && !getenv("LMG_NO_FULL");
+  };
+  if (choose_tile<AK, BKM, ASC>(a) == SEL_WIDE) {
+    if (full(TWide::BM, TWide::BN, TWide::BK)) return launch_cfg<TWide, AK, BKM, ASC, 2, true>(a, st);
+    return launch_cfg<TWide, AK, BKM, ASC, 2>(a, st);
+  }
+  if (full(TSmall::BM, TSmall::BN, TSmall::BK)) return launch_cfg<TSmall, AK, BKM, ASC, 2, true>(a, st);
   return launch_cfg<TSmall, AK, BKM, ASC, 2>(a, st);
 }
 
@@ -435,11 +447,9 @@ int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
   constexpr int STAGE = A_SZ * (V == CV_ADJ ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
   constexpr size_t SMEM = (size_t)CT::STAGES * STAGE * sizeof(double);
   auto kern = conv_gemm<CT, V>;
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-    attr = true;
-  }
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+  if (attr != cudaSuccess) return fail(LMG_ERR_CUDA, cudaGetErrorString(attr));
   if (a.ntasks > 65535) return fail(LMG_ERR_CONFIGURATION, "too many tasks in one launch");
   dim3 grid((a.N + CT::BN - 1) / CT::BN, (a.M + CT::BM - 1) / CT::BM, a.ntasks);
   const int cls = V == CV_FWD ? CLS_GEMM_FWD : (V == CV_ADJ ? CLS_GEMM_ADJ : CLS_GEMM_PG);
@@ -956,6 +966,7 @@ int lmg_abi_version(void) { return 1; }
 unsigned long long lmg_launch_count(void) { return g_launches.load(); }
 
 int lmg_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_rec_mu);
   g_timing = on != 0;
   g_recs.clear();
   g_pool_used = 0;
@@ -1188,7 +1199,15 @@ int lmg_act_deriv(const lmg_system* fine, int B, const double* states, double* D
 int lmg_param_grads(const lmg_system* fine, int B, const double* states, const double* lam,
                     const double* D, double scale, double lr, double* gW, double* gb,
                     void* stream) {
+  return lmg_param_grads_ex(fine, B, states, lam, D, scale, lr, gW, gb, 0, stream);
+}
+
+int lmg_param_grads_ex(const lmg_system* fine, int B, const double* states, const double* lam,
+                       const double* D, double scale, double lr, double* gW, double* gb,
+                       int accumulate, void* stream) {
   TRY(check_sys(fine, B));
+  if (accumulate && (!gW || !gb))
+    return fail(LMG_ERR_CONFIGURATION, "accumulating gradients needs gW and gb buffers");
   if (is_adjoint(*fine)) return fail(LMG_ERR_CONFIGURATION, "param_grads needs the forward system");
   if (!gW && lr == 0.0 && !gb) return LMG_OK;
   const int N = fine->num_layers, q = fine->width;
@@ -1206,11 +1225,13 @@ int lmg_param_grads(const lmg_system* fine, int B, const double* states, const d
     a.x = fine->W; a.x_ts = fine->w_stride;
     a.out = const_cast<double*>(fine->W); a.out_ts = fine->w_stride;
     a.out2 = gW; a.out2_ts = 9LL * g.C * g.C;
+    a.accum = accumulate;
     TRY(launch_conv<CV_PGRAD>(a, g, st));
     return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
       k_conv_bias_grads<<<dim3(g.C, N), 256, 0, st>>>(lam + (int64_t)(N - 1) * BQ, -BQ, D, B, g.C,
                                                      g.HW, fine->step, scale, lr, gb,
-                                                     const_cast<double*>(fine->b), fine->b_stride);
+                                                     const_cast<double*>(fine->b), fine->b_stride,
+                                                     accumulate);
     });
   }
   StepArgs a{};
@@ -1223,11 +1244,13 @@ int lmg_param_grads(const lmg_system* fine, int B, const double* states, const d
   a.out = const_cast<double*>(fine->W); a.out_ts = fine->w_stride;
   a.out2 = gW; a.out2_ts = (int64_t)q * q;
   a.ldc = q;
+  a.accum = accumulate;
   TRY(launch_step(L_PG, a, st));
   const int64_t tot = (int64_t)N * q;
   TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_bias_grads<<<(int)((tot + 255) / 256), 256, 0, st>>>(lam + (int64_t)(N - 1) * BQ, -BQ, D, N, B, q,
                                                          fine->step, scale, lr, gb,
-                                                         const_cast<double*>(fine->b), fine->b_stride); }));
+                                                         const_cast<double*>(fine->b), fine->b_stride,
+                                                         accumulate); }));
   return LMG_OK;
 }
 

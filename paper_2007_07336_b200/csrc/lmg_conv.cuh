@@ -228,7 +228,8 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
           const int tp = m / g.Cp, ci = m % g.Cp;
           if (ci >= g.C) continue;
           const int64_t idx = ((int64_t)tp * g.C + ci) * g.C + n;
-          const double gg = __dmul_rn(__dmul_rn(accv, h), a.scale);
+          double gg = __dmul_rn(__dmul_rn(accv, h), a.scale);
+          if (a.accum && O2) gg = __dadd_rn(O2[idx], gg);
           if (O2) O2[idx] = gg;
           if (a.lr != 0.0) O[idx] = __dadd_rn(X[idx], -__dmul_rn(a.lr, gg));
           continue;

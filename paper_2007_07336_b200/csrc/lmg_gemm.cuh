@@ -59,6 +59,7 @@ struct StepArgs {
   double* out2; int64_t out2_ts;
   int ldc;
   double* part; int64_t part_slot0; int part_ld;
+  int accum;  // E_PGRAD: add the gradient already in out2 (accumulate over batch slices)
 };
 
 __device__ __forceinline__ double act_fwd(int a, double v) {
@@ -85,7 +86,24 @@ __device__ __forceinline__ void cp_async(double* dst, const double* src, bool ok
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(sz));
 }
+// unpredicated form for fully tiled shapes
+template <int VEC>
+__device__ __forceinline__ void cp_async_full(double* dst, const double* src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if (VEC == 2)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+// keep a loop-invariant value in a register: ptxas otherwise rematerializes thread-index
+// arithmetic inside the k-loop (measured: ~30 extra integer instructions per k-tile)
+__device__ __forceinline__ int pin(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
@@ -157,7 +175,7 @@ struct Loader {
       }
       const bool ok = (e < NV) && (mn0 + r < mnlim);
       goff[i] = KMAJ ? (mn0 + r) * ld + kk : kk * ld + mn0 + r;
-      soff[i] = KMAJ ? r * S::LD + kk : kk * S::LD + r;
+      soff[i] = pin(KMAJ ? r * S::LD + kk : kk * S::LD + r);
       kin[i] = kk;
       okmask |= (ok ? 1u : 0u) << i;
     }
@@ -175,6 +193,20 @@ struct Loader {
   }
   __device__ __forceinline__ bool tid_out_of_range(int i) const {
     return (int)(threadIdx.x + i * NT) >= NV;
+  }
+  // fully tiled shapes: running per-thread source pointers, advanced by one k-tile per call
+  const double* cur[IT];
+  __device__ __forceinline__ void init_full() {
+#pragma unroll
+    for (int i = 0; i < IT; ++i) cur[i] = g + goff[i];
+  }
+  __device__ __forceinline__ void load_next(double* sm) {
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      if (IT * NT > NV && tid_out_of_range(i)) continue;
+      cp_async_full<VEC>(sm + soff[i], cur[i]);
+      cur[i] += kadv;
+    }
   }
 };
 
@@ -231,6 +263,7 @@ __device__ __forceinline__ void epilogue(const StepArgs& a, const EpiPtrs& q, do
         const double accv = acc[i][j][e];
         if (EPI == E_PGRAD) {
           double g = __dmul_rn(__dmul_rn(accv, h), a.scale);
+          if (a.accum && q.O2) g = __dadd_rn(q.O2[idx], g);
           if (q.O2) q.O2[idx] = g;
           if (a.lr != 0.0) q.O[idx] = __dadd_rn(q.X[idx], -__dmul_rn(a.lr, g));
           continue;
@@ -271,7 +304,7 @@ __device__ __forceinline__ void epilogue(const StepArgs& a, const EpiPtrs& q, do
   }
 }
 
-template <class T, bool AK, bool BKM, bool ASC, int VEC>
+template <class T, bool AK, bool BKM, bool ASC, int VEC, bool FULL = false>
 __global__ void __launch_bounds__(T::WM* T::WN * 32)
     step_gemm(const StepArgs a) {
   using C = GemmCfg<T, AK, BKM, ASC>;
@@ -302,8 +335,19 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
   lb.init(Bm, a.ldb, n0, a.N, tid);
   Loader<AK, BM, BK, VEC, C::NTHREADS> ld_;
   if (ASC) ld_.init(Ds, a.lda, m0, a.M, tid);
+  if (FULL) {
+    la.init_full();
+    lb.init_full();
+    if (ASC) ld_.init_full();
+  }
   auto load_stage = [&](int s, int kt) {
     double* base = smem + s * C::STAGE;
+    if (FULL) {  // loads are issued for kt = 0, 1, 2, ... in order
+      la.load_next(base);
+      if (ASC) ld_.load_next(base + C::A_SZ);
+      lb.load_next(base + C::A_SZ * (ASC ? 2 : 1));
+      return;
+    }
     const int k0 = kt * BK;
     const bool kfull = kfull_all || (k0 + BK <= a.K);
     la.load(base, kt, k0, a.K, kfull);
@@ -319,6 +363,9 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
 
   const int wm0 = wm * C::WTM, wn0 = wn * C::WTN;
   const int fr = lane >> 2, fk = lane & 3;
+  constexpr int LDA_ = TileShape<AK, BM, BK>::LD, LDB_ = TileShape<BKM, BN, BK>::LD;
+  const int a_thr = pin(AK ? (wm0 + fr) * LDA_ + fk : fk * LDA_ + wm0 + fr);
+  const int b_thr = pin(BKM ? (wn0 + fr) * LDB_ + fk : fk * LDB_ + wn0 + fr);
 
   for (int kt = 0; kt < KT; ++kt) {
     cp_wait<STAGES - 2>();
@@ -332,14 +379,16 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     const double* Dsm = As + C::A_SZ;
     const double* Bs = As + C::A_SZ * (ASC ? 2 : 1);
     double af[2][C::MT], bf[2][C::NTF];
+    // per-thread fragment offsets are loop invariant (a_thr / b_thr); only constants vary below
     auto ldfrag = [&](int buf, int kk) {
 #pragma unroll
       for (int i = 0; i < C::MT; ++i) {
-        af[buf][i] = frag<AK, BM, BK>(As, wm0 + i * 8 + fr, kk + fk);
-        if (ASC) af[buf][i] = __dmul_rn(af[buf][i], frag<AK, BM, BK>(Dsm, wm0 + i * 8 + fr, kk + fk));
+        const int o = a_thr + (AK ? i * 8 * LDA_ + kk : kk * LDA_ + i * 8);
+        af[buf][i] = As[o];
+        if (ASC) af[buf][i] = __dmul_rn(af[buf][i], Dsm[o]);
       }
 #pragma unroll
-      for (int j = 0; j < C::NTF; ++j) bf[buf][j] = frag<BKM, BN, BK>(Bs, wn0 + j * 8 + fr, kk + fk);
+      for (int j = 0; j < C::NTF; ++j) bf[buf][j] = Bs[b_thr + (BKM ? j * 8 * LDB_ + kk : kk * LDB_ + j * 8)];
     };
     ldfrag(0, 0);
 #pragma unroll

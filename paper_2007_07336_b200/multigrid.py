@@ -308,14 +308,24 @@ def initial_guess(level, source):
     return np.tile(np.asarray(source[0], dtype=np.float64), (n, 1))
 
 
+def solver_workspace(view: SystemView, nlevels: int, c: int, B: int, device, adjoint_D=None):
+    """A private device workspace for solve_device (concurrent solves need their own)."""
+    t = require_cuda()
+    nbytes = _lib.load().lmg_solver_workspace(view.desc(adjoint_D), nlevels, c, B)
+    return t.empty(nbytes // 8 + 32, dtype=t.float64, device=device), nbytes
+
+
 def solve_device(view: SystemView, nlevels: int, c: int, src, states, *, src_mode: int,
-                 use_initial: bool, tol: float, max_cycles: int, adjoint_D=None):
+                 use_initial: bool, tol: float, max_cycles: int, adjoint_D=None, work=None):
     """Core batched solve on device tensors (states (N, B, q) updated in place).
     Returns (hist (cycles+1, B) numpy, cycles (B,), converged (B,))."""
     t = require_cuda()
     B = states.shape[1]
     desc = view.desc(adjoint_D)
-    work, nbytes = _Workspace.get(desc, nlevels, c, B, states.device)
+    if work is None:
+        work, nbytes = _Workspace.get(desc, nlevels, c, B, states.device)
+    else:
+        work, nbytes = work
     hist = np.full((max_cycles + 1, B), np.nan)
     cyc = np.zeros(B, dtype=np.int32)
     conv = np.zeros(B, dtype=np.int32)

@@ -152,7 +152,8 @@ class AdjointResult:
 
 def backward(dnet: DeviceNet, U, X, labels, *, adjoint: str = "sequential", coarsening: int = 4,
              threshold: int | None = None, tol: float = 1e-9, max_cycles: int = 50,
-             scale: float = 1.0, lr: float = 0.0, want_grads: bool = True, lam_buf=None, D_buf=None):
+             scale: float = 1.0, lr: float = 0.0, want_grads: bool = True, lam_buf=None, D_buf=None,
+             block_grads: bool = True, work=None):
     """Loss + adjoint + parameter gradients for a batch at forward states U (N, B, q).
 
     Parameter gradients are summed over the batch and multiplied by ``scale`` (1/B gives the
@@ -187,7 +188,7 @@ def backward(dnet: DeviceNet, U, X, labels, *, adjoint: str = "sequential", coar
         nlev = _levels_for(N, coarsening, threshold)
         hist, cyc, conv = solve_device(view, nlev, coarsening, g_final, lam, src_mode=_lib.SRC_HEAD,
                                        use_initial=False, tol=tol, max_cycles=max_cycles,
-                                       adjoint_D=D)
+                                       adjoint_D=D, work=work)
         r.hist, r.cycles, r.converged = hist, cyc, conv
     else:
         raise ConfigurationError(f"adjoint must be 'sequential' or 'fas', got {adjoint!r}")
@@ -200,11 +201,12 @@ def backward(dnet: DeviceNet, U, X, labels, *, adjoint: str = "sequential", coar
     if want_grads:
         gW = t.empty_like(dnet.stack.W)
         gb = t.empty_like(dnet.stack.b)
-    _lib.call("lmg_param_grads", view.desc(), B, U.data_ptr(), lam.data_ptr(), D.data_ptr(),
-              float(scale), float(lr), None if gW is None else gW.data_ptr(),
-              None if gb is None else gb.data_ptr(), st)
+    if block_grads:
+        _lib.call("lmg_param_grads", view.desc(), B, U.data_ptr(), lam.data_ptr(), D.data_ptr(),
+                  float(scale), float(lr), None if gW is None else gW.data_ptr(),
+                  None if gb is None else gb.data_ptr(), st)
     _, gWo, gbo = _dense_vjp(dnet.Wo, dnet.bo, dnet.open_act, X, lam0, want_gx=False)
-    if lr != 0.0:
+    if lr != 0.0 and block_grads:
         for p, g in ((dnet.Wo, gWo), (dnet.bo, gbo), (dnet.Wr, gWr), (dnet.br, gbr)):
             p.sub_(g * (scale * lr))
     r.loss, r.logits, r.final, r.lam, r.lam0, r.D = loss, logits, final, lam, lam0, D
@@ -341,7 +343,7 @@ class DeviceTrainer:
     def __init__(self, dnet: DeviceNet, *, coarsening: int = 4, threshold: int | None = None,
                  tol: float = 1e-9, max_cycles: int = 50, adjoint: str = "fas",
                  adj_tol: float | None = None, adj_max_cycles: int | None = None,
-                 learning_rate: float = 0.1):
+                 learning_rate: float = 0.1, split: int = 1):
         from .multigrid import _levels_for
 
         self.dnet = dnet
@@ -353,7 +355,9 @@ class DeviceTrainer:
         self.adj_tol = tol if adj_tol is None else adj_tol
         self.adj_max_cycles = max_cycles if adj_max_cycles is None else adj_max_cycles
         self.lr = learning_rate
+        self.split = max(1, int(split))
         self._bufs = None
+        self._slices = None
 
     def _buffers(self, B, device):
         t = require_cuda()
@@ -376,9 +380,108 @@ class DeviceTrainer:
         return U, hist, cyc, conv
 
     def step(self, X, labels) -> StepResult:
+        if self.split > 1 and X.shape[0] >= 2 * self.split:
+            return self._step_split(X, labels)
         U, hist, cyc, conv = self.forward(X)
         _, lam, D = self._buffers(X.shape[0], X.device)
         r = backward(self.dnet, U, X, labels, adjoint=self.adjoint, coarsening=self.c,
                      threshold=self.threshold, tol=self.adj_tol, max_cycles=self.adj_max_cycles,
                      scale=1.0 / X.shape[0], lr=self.lr, want_grads=False, lam_buf=lam, D_buf=D)
         return StepResult(r.loss, hist, cyc, conv, r.hist, r.cycles, r.converged)
+
+    # -- batch slices on concurrent streams ------------------------------------------------------
+    def _slice_state(self, B, device):
+        """Per-slice buffers, workspaces and streams (samples are independent: every state is
+        bitwise the unsplit batch's; the slices' block gradients are accumulated in one pass)."""
+        t = require_cuda()
+        key = (B, str(device), self.split)
+        if self._slices is not None and self._slices[0] == key:
+            return self._slices[1]
+        from .multigrid import solver_workspace
+
+        bounds = np.linspace(0, B, self.split + 1).astype(int)
+        view = self.dnet._lmg_view()
+        sl = []
+        for i in range(self.split):
+            lo, hi = int(bounds[i]), int(bounds[i + 1])
+            shape = (self.dnet.num_blocks, hi - lo, self.dnet.width)
+            U = t.empty(shape, dtype=t.float64, device=device)
+            lam = t.empty(shape, dtype=t.float64, device=device)
+            D = t.empty(shape, dtype=t.float64, device=device)
+            wf = solver_workspace(view, self.nlevels, self.c, hi - lo, device)
+            wa = solver_workspace(view, self.nlevels, self.c, hi - lo, device, adjoint_D=D)
+            sl.append(dict(lo=lo, hi=hi, U=U, lam=lam, D=D, wf=wf, wa=wa,
+                           stream=t.cuda.Stream(device=device)))
+        gW = t.empty_like(self.dnet.stack.W)
+        gb = t.empty_like(self.dnet.stack.b)
+        self._slices = (key, (sl, gW, gb))
+        return sl, gW, gb
+
+    def _step_split(self, X, labels) -> StepResult:
+        import threading
+
+        t = require_cuda()
+        B = X.shape[0]
+        sl, gW, gb = self._slice_state(B, X.device)
+        dnet = self.dnet
+        view = dnet._lmg_view()
+        main = t.cuda.current_stream(X.device)
+        out = [None] * len(sl)
+        err = []
+
+        def run(i):
+            s = sl[i]
+            try:
+                s["stream"].wait_stream(main)
+                with t.cuda.stream(s["stream"]):
+                    Xi, li = X[s["lo"]:s["hi"]], labels[s["lo"]:s["hi"]]
+                    f0 = _dense_apply(dnet.Wo, dnet.bo, dnet.open_act, Xi)
+                    hist, cyc, conv = solve_device(view, self.nlevels, self.c, f0, s["U"],
+                                                   src_mode=_lib.SRC_HEAD, use_initial=False,
+                                                   tol=self.tol, max_cycles=self.max_cycles,
+                                                   work=s["wf"])
+                    r = backward(dnet, s["U"], Xi, li, adjoint=self.adjoint, coarsening=self.c,
+                                 threshold=self.threshold, tol=self.adj_tol,
+                                 max_cycles=self.adj_max_cycles, scale=1.0 / B, lr=0.0,
+                                 want_grads=False, lam_buf=s["lam"], D_buf=s["D"],
+                                 block_grads=False, work=s["wa"])
+                    out[i] = (hist, cyc, conv, r)
+            except Exception as e:  # pragma: no cover - surfaced below
+                err.append(e)
+
+        threads = [threading.Thread(target=run, args=(i,)) for i in range(len(sl))]
+        for th in threads:
+            th.start()
+        for th in threads:
+            th.join()
+        if err:
+            raise err[0]
+        for s in sl:
+            main.wait_stream(s["stream"])
+        st = _lib.stream_handle()
+        for i, s in enumerate(sl):  # block gradients accumulated over slices, SGD on the last
+            last = i == len(sl) - 1
+            _lib.call("lmg_param_grads_ex", view.desc(), s["hi"] - s["lo"], s["U"].data_ptr(),
+                      s["lam"].data_ptr(), s["D"].data_ptr(), 1.0 / B, float(self.lr) if last else 0.0,
+                      gW.data_ptr(), gb.data_ptr(), int(i > 0), st)
+        rs = [o[3] for o in out]
+        if self.lr:
+            scale = 1.0 / B
+            for p, name in ((dnet.Wo, "gWo"), (dnet.bo, "gbo"), (dnet.Wr, "gWr"), (dnet.br, "gbr")):
+                g = getattr(rs[0], name)
+                for r in rs[1:]:
+                    g = g + getattr(r, name)
+                p.sub_(g * (scale * self.lr))
+        cat = lambda a: np.concatenate(a, axis=-1)  # noqa: E731
+        nmax = max(o[0].shape[0] for o in out)
+        pad = lambda h: np.vstack([h, np.full((nmax - h.shape[0], h.shape[1]), np.nan)])  # noqa: E731
+        loss = t.cat([r.loss for r in rs])
+        adj = rs[0].hist is not None
+        if adj:
+            amax = max(r.hist.shape[0] for r in rs)
+            apad = lambda h: np.vstack([h, np.full((amax - h.shape[0], h.shape[1]), np.nan)])  # noqa: E731
+        return StepResult(loss, cat([pad(o[0]) for o in out]), cat([o[1] for o in out]),
+                          cat([o[2] for o in out]),
+                          cat([apad(r.hist) for r in rs]) if adj else None,
+                          cat([r.cycles for r in rs]) if adj else None,
+                          cat([r.converged for r in rs]) if adj else None)

@@ -257,3 +257,26 @@ def test_conv_transform_and_vjp_against_oracle():
     ow, ob = lev.param_grads(0, X, G * D)
     assert np.max(np.abs(gw - ow)) <= 1e-12 * np.max(np.abs(ow))
     assert np.max(np.abs(gb - ob)) <= 1e-12 * np.max(np.abs(ob))
+
+
+def test_split_batch_step_matches_unsplit():
+    """DeviceTrainer(split=2): batch slices on concurrent streams -- per-sample solves are bitwise
+    the unsplit ones; accumulated gradients and the SGD step agree within rounding."""
+    N, q, B = 64, 32, 8
+    X = dev(P.random_batch(q, [2, N, q], B))
+    labels = dev(np.arange(B) % 10)
+    res = {}
+    for split in (1, 2):
+        d = P.device_network(N, q, [2, N, q])
+        tr = P.DeviceTrainer(d, coarsening=4, tol=1e-10, max_cycles=50, adjoint="fas",
+                             learning_rate=0.1, split=split)
+        r = tr.step(X, labels)
+        res[split] = (r, d.stack.W.cpu().numpy(), d.Wo.cpu().numpy())
+    r1, W1, Wo1 = res[1]
+    r2, W2, Wo2 = res[2]
+    h1 = r1.fwd_hist[: r1.fwd_cycles.max() + 1]
+    h2 = r2.fwd_hist[: r2.fwd_cycles.max() + 1]
+    assert np.array_equal(h1, h2, equal_nan=True)
+    assert np.array_equal(r1.loss.cpu().numpy(), r2.loss.cpu().numpy())
+    assert np.max(np.abs(W1 - W2)) <= 1e-14
+    assert np.max(np.abs(Wo1 - Wo2)) <= 1e-14
