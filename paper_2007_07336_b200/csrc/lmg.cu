@@ -341,6 +341,7 @@ enum Layout { L_FWD = 0, L_ADJ = 1, L_PG = 2 };
 //   single-task serial step:          TSmall 18.9 us    TWide 24.3   64x64 47.9
 using TSmall = Tile<32, 32, 16, 2, 2, 4>;  // 4 warps of 16x16, ~5 CTAs/SM
 using TWide = Tile<32, 64, 16, 2, 4, 4>;   // 8 warps of 16x16
+using TTiny = Tile<16, 32, 16, 1, 2, 4>;   // batches <= 16: 2 warps of 16x16, no wasted rows
 
 template <class T, bool AK, bool BKM, bool ASC, int VEC, bool FULL = false>
 int launch_cfg(const StepArgs& a, cudaStream_t st) {
@@ -363,13 +364,14 @@ int n_tiles(int N) { return (N + TSmall::BN - 1) / TSmall::BN; }
 
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-enum TileSel { SEL_AUTO = 0, SEL_SMALL = 1, SEL_WIDE = 2 };
+enum TileSel { SEL_AUTO = 0, SEL_SMALL = 1, SEL_WIDE = 2, SEL_TINY = 3 };
 
 int tile_override() {
   static int v = [] {
     const char* e = getenv("LMG_TILE");
     if (e && !strcmp(e, "small")) return (int)SEL_SMALL;
     if (e && !strcmp(e, "wide")) return (int)SEL_WIDE;
+    if (e && !strcmp(e, "tiny")) return (int)SEL_TINY;
     return (int)SEL_AUTO;
   }();
   return v;
@@ -385,6 +387,7 @@ int choose_tile(const StepArgs& a) {
   int o = tile_override();
   if (o != SEL_AUTO) return o;
   const bool adj = AK && !BKM;
+  if (AK && a.M <= 16) return SEL_TINY;  // step launches with a small batch (M = B)
   if (adj && ctas_for(a, TWide::BM, TWide::BN) >= 2 * 148) return SEL_WIDE;
   return SEL_SMALL;
 }
@@ -395,7 +398,12 @@ int launch_layout(const StepArgs& a, bool v2, cudaStream_t st) {
   auto full = [&](int BM, int BN, int BK) {
     return a.M % BM == 0 && a.N % BN == 0 && a.K % BK == 0 && !getenv("LMG_NO_FULL");
   };
-  if (choose_tile<AK, BKM, ASC>(a) == SEL_WIDE) {
+  const int sel = choose_tile<AK, BKM, ASC>(a);
+  if (sel == SEL_TINY) {
+    if (full(TTiny::BM, TTiny::BN, TTiny::BK)) return launch_cfg<TTiny, AK, BKM, ASC, 2, true>(a, st);
+    return launch_cfg<TTiny, AK, BKM, ASC, 2>(a, st);
+  }
+  if (sel == SEL_WIDE) {
     if (full(TWide::BM, TWide::BN, TWide::BK)) return launch_cfg<TWide, AK, BKM, ASC, 2, true>(a, st);
     return launch_cfg<TWide, AK, BKM, ASC, 2>(a, st);
   }
@@ -1116,16 +1124,46 @@ int lmg_mg_cycle(const lmg_system* fine, int nlevels, int c, int B, double* stat
                norms ? norms : ws.norms, S_(stream));
 }
 
+int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
+             const double* src, int src_mode, int use_initial, double tol, int max_cycles,
+             double* hist_host, int32_t* cycles_host, int32_t* converged_host, void* work,
+             size_t work_bytes, cudaStream_t st);
+
 int lmg_solve(const lmg_system* fine, int nlevels, int c, int B, double* states,
               const double* src, int src_mode, int use_initial, double tol, int max_cycles,
               double* hist_host, int32_t* cycles_host, int32_t* converged_host, void* work,
               size_t work_bytes, void* stream) {
+  cudaStream_t st = S_(stream);
+  if (st != nullptr && st != cudaStreamLegacy)
+    return solve_on(fine, nlevels, c, B, states, src, src_mode, use_initial, tol, max_cycles,
+                    hist_host, cycles_host, converged_host, work, work_bytes, st);
+  // graphs cannot be captured on the legacy default stream: run on a private stream of this
+  // thread, ordered after / before the caller's stream by events
+  static thread_local cudaStream_t own = nullptr;
+  static thread_local cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  if (!own) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+  }
+  CUDA_TRY(cudaEventRecord(ev_in, st));
+  CUDA_TRY(cudaStreamWaitEvent(own, ev_in, 0));
+  int rc = solve_on(fine, nlevels, c, B, states, src, src_mode, use_initial, tol, max_cycles,
+                    hist_host, cycles_host, converged_host, work, work_bytes, own);
+  CUDA_TRY(cudaEventRecord(ev_out, own));
+  CUDA_TRY(cudaStreamWaitEvent(st, ev_out, 0));
+  return rc;
+}
+
+int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
+             const double* src, int src_mode, int use_initial, double tol, int max_cycles,
+             double* hist_host, int32_t* cycles_host, int32_t* converged_host, void* work,
+             size_t work_bytes, cudaStream_t st) {
   TRY(check_sys(fine, B));
   if (!(std::isfinite(tol) && tol > 0))
     return fail(LMG_ERR_CONFIGURATION, "tolerance must be a finite positive number");
   if (max_cycles < 1) return fail(LMG_ERR_CONFIGURATION, "max_cycles must be >= 1");
   TRY(check_levels(*fine, nlevels, c));
-  cudaStream_t st = S_(stream);
   Workspace ws;
   layout_ws(*fine, nlevels, c, B, reinterpret_cast<char*>(work), &ws);
   if (work_bytes < ws.bytes) return fail(LMG_ERR_CONFIGURATION, "workspace too small");
@@ -1157,9 +1195,39 @@ int lmg_solve(const lmg_system* fine, int nlevels, int c, int B, double* states,
   for (int b = 0; b < B && ndone < B; ++b)
     if (done[b]) TRY(park(b));
 
+  // Cycles 2.. issue an identical launch sequence: capture it once as a CUDA graph and replay
+  // it (one host call per cycle instead of ~100 launches).  Not under per-launch timing.
+  const bool use_graph = !g_timing && !getenv("LMG_NO_GRAPH");
+  cudaGraphExec_t gexec = nullptr;
+  unsigned long long graph_launches = 0;
+  struct GraphGuard {
+    cudaGraphExec_t* g;
+    ~GraphGuard() {
+      if (*g) cudaGraphExecDestroy(*g);
+    }
+  } guard{&gexec};
   int cyc = 0;
   while (ndone < B && cyc < max_cycles) {
-    TRY(cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, cyc > 0));
+    if (use_graph && cyc > 0) {
+      if (!gexec) {
+        cudaGraph_t graph;
+        const unsigned long long n0 = g_launches.load();
+        CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        int rc = cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, true);
+        cudaError_t ce = cudaStreamEndCapture(st, &graph);
+        if (rc != LMG_OK) return rc;
+        if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+        graph_launches = g_launches.load() - n0;
+        ce = cudaGraphInstantiate(&gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+        g_launches -= graph_launches;  // counted per replay below
+      }
+      CUDA_TRY(cudaGraphLaunch(gexec, st));
+      g_launches += graph_launches;
+    } else {
+      TRY(cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, cyc > 0));
+    }
     ++cyc;
     CUDA_TRY(cudaMemcpyAsync(nrm.data(), ws.norms, B * sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
