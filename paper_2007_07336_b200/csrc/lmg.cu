@@ -411,6 +411,53 @@ int launch_layout(const StepArgs& a, bool v2, cudaStream_t st) {
   return launch_cfg<TSmall, AK, BKM, ASC, 2>(a, st);
 }
 
+// ---- split-K cluster kernel for serial single-task steps ----------------------------------------
+template <class T, bool AK, bool BKM, bool ASC>
+int launch_serial_cfg(const StepArgs& a, int KS, cudaStream_t st) {
+  using C = GemmCfg<T, AK, BKM, ASC>;
+  auto kern = serial_gemm<T, AK, BKM, ASC>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (attr != cudaSuccess) return fail(LMG_ERR_CUDA, cudaGetErrorString(attr));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.N / C::BN, a.M / C::BM, KS);
+  cfg.blockDim = dim3(C::NTHREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = KS;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const int cls = AK ? (BKM ? CLS_GEMM_FWD : CLS_GEMM_ADJ) : CLS_GEMM_PG;
+  const double flops = (double)a.M * a.N * (2.0 * a.K + 5.0);
+  const double bytes = 8.0 * ((double)a.N * a.K + (double)a.M * a.K + 2.0 * a.M * a.N);
+  return launch(cls, flops, bytes, st, [&] { cudaLaunchKernelEx(&cfg, kern, a); });
+}
+
+// returns LMG_OK after launching, or -1 if the step is not eligible (caller falls back)
+int launch_serial(Layout L, const StepArgs& a, cudaStream_t st) {
+  if (getenv("LMG_NO_SPLITK")) return -1;
+  if (a.ntasks != 1 || (a.epi != E_PROP && a.epi != E_ADV) || L == L_PG) return -1;
+  if (!aligned16(a.A) || !aligned16(a.Bm) || !aligned16(a.Ds) || (a.lda | a.ldb | a.K | a.N) & 1)
+    return -1;
+  const bool tiny = a.M <= 16;
+  const int BM = tiny ? TTiny::BM : TSmall::BM, BN = tiny ? TTiny::BN : TSmall::BN, BK = 16;
+  if (a.M % BM || a.N % BN || a.K % BK) return -1;
+  const int64_t base = (int64_t)(a.N / BN) * (a.M / BM);
+  int KS = 1;
+  while (KS < 8 && base * KS * 2 <= 4 * 148 && (a.K / BK) % (KS * 2) == 0) KS *= 2;
+  if (KS == 1) return -1;
+  const bool adj = (L == L_ADJ);
+  if (tiny)
+    return adj ? launch_serial_cfg<TTiny, true, false, true>(a, KS, st)
+               : launch_serial_cfg<TTiny, true, true, false>(a, KS, st);
+  return adj ? launch_serial_cfg<TSmall, true, false, true>(a, KS, st)
+             : launch_serial_cfg<TSmall, true, true, false>(a, KS, st);
+}
+
 int launch_step(Layout L, const StepArgs& a, cudaStream_t st) {
   if (a.ntasks <= 0 || a.M <= 0 || a.N <= 0) return LMG_OK;
   if (a.ntasks > 65535) return fail(LMG_ERR_CONFIGURATION, "too many tasks in one launch");
@@ -514,6 +561,7 @@ struct Fam {
   double* out = nullptr; int64_t out_ts = 0;
   double* out2 = nullptr; int64_t out2_ts = 0;
   double* part = nullptr; int64_t slot0 = 0;
+  bool serial = false;  // an inherently serial single-task step: split-K cluster kernel
 };
 
 int family(const lmg_system& S, int B, int epi, const Fam& f, cudaStream_t st) {
@@ -550,11 +598,19 @@ int family(const lmg_system& S, int B, int epi, const Fam& f, cudaStream_t st) {
     a.act = LMG_ACT_IDENTITY;
     a.bias = nullptr;
     a.Ds = S.D + (int64_t)f.blk0 * S.d_stride; a.Ds_ts = (int64_t)f.blk_step * S.d_stride;
+    if (f.serial) {
+      const int r = launch_serial(L_ADJ, a, st);
+      if (r >= 0) return r;
+    }
     return launch_step(L_ADJ, a, st);
   }
   a.act = S.act;
   a.bias = S.b ? S.b + (int64_t)f.blk0 * S.b_stride : nullptr;
   a.bias_ts = (int64_t)f.blk_step * S.b_stride;
+  if (f.serial) {
+    const int r = launch_serial(L_FWD, a, st);
+    if (r >= 0) return r;
+  }
   return launch_step(L_FWD, a, st);
 }
 
@@ -582,6 +638,7 @@ int seq_forward(const lmg_system& S, int B, const double* src, int mode, double*
     f.x = U + (int64_t)(j - 1) * BQ;
     f.s = src_row(src, mode, BQ, j);
     f.out = U + (int64_t)j * BQ;
+    f.serial = true;
     TRY(family(S, B, E_PROP, f, st));
   }
   return LMG_OK;
@@ -1016,6 +1073,7 @@ int lmg_propagate(const lmg_system* sys, int B, const double* u_start, const dou
     f.x = j == start ? u_start : out + (int64_t)(j - 1 - start) * BQ;
     f.s = src_row(src, src_mode, BQ, j);
     f.out = out + (int64_t)(j - start) * BQ;
+    f.serial = true;
     TRY(family(*sys, B, E_PROP, f, S_(stream)));
   }
   return LMG_OK;

@@ -448,3 +448,130 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
 }
 
 }  // namespace lmg
+
+// ------------------------------------------------------------------------------------------------
+// Split-K layer step for inherently serial steps (coarsest exact solve, sequential_forward, the
+// serial adjoint): one step's K range is split over the KS CTAs of a thread-block cluster
+// (gridDim.z == cluster z == KS), each accumulates its slice with the same DMMA mainloop, then the
+// partial tiles are summed through distributed shared memory in fixed rank order (deterministic)
+// and the E_PROP / E_ADV epilogue is applied, each CTA finishing 1/KS of the tile.  Fully tiled
+// shapes only (M % BM == N % BN == (K/KS) % BK == 0).
+#include <cooperative_groups.h>
+
+namespace lmg {
+
+__device__ __forceinline__ double epi_point(int epi, int actk, double h, double pre, double xv,
+                                            double sv) {
+  const double v = act_fwd(actk, pre);
+  const double adv = __dadd_rn(xv, __dmul_rn(h, v));
+  return epi == E_ADV ? adv : __dadd_rn(sv, adv);
+}
+
+template <class T, bool AK, bool BKM, bool ASC>
+__global__ void __launch_bounds__(T::WM* T::WN * 32)
+    serial_gemm(const StepArgs a) {
+  namespace cg = cooperative_groups;
+  using C = GemmCfg<T, AK, BKM, ASC>;
+  constexpr int BM = C::BM, BN = C::BN, BK = C::BK, WN = C::WN, STAGES = C::STAGES;
+  extern __shared__ __align__(16) double smem[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int KS = gridDim.z, rank = blockIdx.z;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  const int KT = a.K / BK / KS, kt0 = rank * KT;
+
+  double acc[C::MT][C::NTF][2];
+#pragma unroll
+  for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NTF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  Loader<AK, BM, BK, 2, C::NTHREADS> la, ld_;
+  Loader<BKM, BN, BK, 2, C::NTHREADS> lb;
+  la.init(a.A, a.lda, m0, a.M, tid);
+  lb.init(a.Bm, a.ldb, n0, a.N, tid);
+  if (ASC) ld_.init(a.Ds, a.lda, m0, a.M, tid);
+  la.init_full();
+  lb.init_full();
+  if (ASC) ld_.init_full();
+#pragma unroll
+  for (int i = 0; i < la.IT; ++i) la.cur[i] += kt0 * la.kadv;
+#pragma unroll
+  for (int i = 0; i < lb.IT; ++i) lb.cur[i] += kt0 * lb.kadv;
+  if (ASC) {
+#pragma unroll
+    for (int i = 0; i < ld_.IT; ++i) ld_.cur[i] += kt0 * ld_.kadv;
+  }
+  auto load_stage = [&](int s) {
+    double* base = smem + s * C::STAGE;
+    la.load_next(base);
+    if (ASC) ld_.load_next(base + C::A_SZ);
+    lb.load_next(base + C::A_SZ * (ASC ? 2 : 1));
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) load_stage(s);
+    cp_commit();
+  }
+  const int wm0 = wm * C::WTM, wn0 = wn * C::WTN;
+  const int fr = lane >> 2, fk = lane & 3;
+  constexpr int LDA_ = TileShape<AK, BM, BK>::LD, LDB_ = TileShape<BKM, BN, BK>::LD;
+  const int a_thr = AK ? (wm0 + fr) * LDA_ + fk : fk * LDA_ + wm0 + fr;
+  const int b_thr = BKM ? (wn0 + fr) * LDB_ + fk : fk * LDB_ + wn0 + fr;
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    if (kt + STAGES - 1 < KT) load_stage((kt + STAGES - 1) % STAGES);
+    cp_commit();
+    const double* As = smem + (kt % STAGES) * C::STAGE;
+    const double* Dsm = As + C::A_SZ;
+    const double* Bs = As + C::A_SZ * (ASC ? 2 : 1);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[C::MT], bf[C::NTF];
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i) {
+        const int o = a_thr + (AK ? i * 8 * LDA_ + kk : kk * LDA_ + i * 8);
+        af[i] = As[o];
+        if (ASC) af[i] = __dmul_rn(af[i], Dsm[o]);
+      }
+#pragma unroll
+      for (int j = 0; j < C::NTF; ++j) bf[j] = Bs[b_thr + (BKM ? j * 8 * LDB_ + kk : kk * LDB_ + j * 8)];
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NTF; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();
+  // partial tile -> own smem [BM][BN]
+  double* part = smem;
+#pragma unroll
+  for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NTF; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        part[(wm0 + i * 8 + fr) * BN + wn0 + j * 8 + 2 * fk + e] = acc[i][j][e];
+  cluster.sync();
+  // reduce a 1/KS share of the tile over the cluster in rank order, then the epilogue
+  const int per = (BM * BN + KS - 1) / KS;
+  const int e0 = rank * per, e1 = min(BM * BN, e0 + per);
+  const double* X = a.x;
+  const double* S = a.s;
+  for (int e = e0 + tid; e < e1; e += C::NTHREADS) {
+    double sum = 0.0;
+    for (int r = 0; r < KS; ++r) sum += cluster.map_shared_rank(part, r)[e];
+    const int m = m0 + e / BN, n = n0 + e % BN;
+    const int64_t idx = (int64_t)m * a.ldc + n;
+    double pre = sum;
+    if (a.bias) pre = __dadd_rn(pre, a.bias[n]);
+    a.out[idx] = epi_point(a.epi, a.act, a.h, pre, X[idx], S ? S[idx] : 0.0);
+  }
+  cluster.sync();
+}
+
+}  // namespace lmg
