@@ -167,13 +167,16 @@ int lmg_param_grads_ex(const lmg_system* fine, int B, const double* states, cons
  * given, the first F-sweep step is a copy instead of a launch (bitwise identical). */
 int lmg_local_fcf_a(const lmg_system* sys, int B, int c, double* U, const double* src,
                     int src_mode, int is_first, int has_next, const double* Q, void* stream);
+/* advH (optional, nb rows): receives U[kc] + H F_H(U[kc]) (H = c h) from the second sweep's first
+ * step -- the same pre-activation -- so lmg_local_coarse_source needs no GEMM of its own. */
 int lmg_local_fcf_b(const lmg_system* sys, int B, int c, double* U, const double* src,
-                    int src_mode, double* P, int has_next, double* adv_out, void* stream);
+                    int src_mode, double* P, int has_next, double* adv_out, double* advH,
+                    void* stream);
 int lmg_halo_finish(const double* s0, const double* adv_in, double* out, int64_t len, void* stream);
 int lmg_local_coarse_source(const lmg_system* sys, int B, int c, const double* U,
                             const double* src, int src_mode, const double* P,
                             const double* adv_in, int is_first, double* SH, double* V,
-                            void* stream);
+                            const double* advH, void* stream);
 int lmg_local_correct(int n_blocks, int B, int q, int c, double* U, const double* V, void* stream);
 size_t lmg_local_workspace(int L, int B, int q);
 int lmg_local_residual_post(const lmg_system* sys, int B, int c, const double* U,

@@ -76,14 +76,19 @@ class NumpyOps:
         if is_first:
             u[0] = sr(0)
 
-    def fcf_b(self, lv, U, S, smode, P, has_next, adv_out):
+    def fcf_b(self, lv, U, S, smode, P, has_next, adv_out, advH=None):
         lev, u, c, nb = lv.desc(), _a(U), lv.c, lv.nb
         h, sr = lev.step, self._src(S, smode)
         p = _a(P)
+        hc = lev.coarsen(c)
+        ah = _a(advH)
         for i in range(1, c):
             for k in range(nb):
                 j = k * c + i
-                u[j] = sr(j) + (u[j - 1] + h * lev.F(j - 1, u[j - 1]))
+                fv = lev.F(j - 1, u[j - 1])
+                if i == 1 and ah is not None:  # coarse advance from the same F evaluation
+                    ah[k] = u[j - 1] + hc.step * fv
+                u[j] = sr(j) + (u[j - 1] + h * fv)
         K1 = nb - 1 + int(has_next)
         for k in range(1, K1 + 1):
             j = k * c
@@ -96,13 +101,14 @@ class NumpyOps:
     def halo_finish(self, s0, adv, out):
         _a(out)[...] = (0.0 if s0 is None else _a(s0)) + _a(adv)
 
-    def coarse_source(self, lv, U, S, smode, P, adv_in, is_first, SH, V):
+    def coarse_source(self, lv, U, S, smode, P, adv_in, is_first, SH, V, advH=None):
         lev, u, c, nb = lv.desc(), _a(U), lv.c, lv.nb
         hc = lev.coarsen(c)
         p, sh, v, sr = _a(P), _a(SH), _a(V), self._src(S, smode)
+        ah = _a(advH)
         for n in range(1, nb):
             x, y = u[(n - 1) * c], u[n * c]
-            adv = x + hc.step * hc.F(n - 1, x)
+            adv = ah[n - 1] if ah is not None else x + hc.step * hc.F(n - 1, x)
             sh[n] = (y - adv) + (p[n] - y)
             if v is not None:
                 v[n] = y

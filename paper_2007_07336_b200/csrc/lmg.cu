@@ -161,6 +161,22 @@ __global__ void k_halo_finish(const double* __restrict__ s0, const double* __res
     out[i] = __dadd_rn(s0 ? s0[i] : 0.0, adv[i]);
 }
 
+// coarse FAS source rows n >= 1 from the advance computed in the F sweep:
+//   S_H[n] = (U[nc] - advH[n-1]) + (P[n] - U[nc]),  V[n] = U[nc]      (multigrid.py:142)
+__global__ void k_coarse_from_adv(const double* __restrict__ Uc, int64_t u_ts,
+                                  const double* __restrict__ adv, const double* __restrict__ P,
+                                  double* __restrict__ SH, double* __restrict__ V, int64_t nrows,
+                                  int64_t len) {
+  const int64_t total = nrows * len;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / len, i = e - r * len;
+    const double y = Uc[r * u_ts + i];
+    SH[e] = __dadd_rn(__dadd_rn(y, -adv[e]), __dadd_rn(P[e], -y));
+    if (V) V[e] = y;
+  }
+}
+
 // first coarse-source row of a non-first rank: S_H[0] = (U[0] - adv_in) + (P[0] - U[0]), where
 // adv_in = U_prev + H*F(U_prev) came from the previous rank (multigrid.py:142, network.py:138)
 __global__ void k_row0_coarse_halo(const double* __restrict__ U0, const double* __restrict__ adv,
@@ -562,6 +578,7 @@ struct Fam {
   double* out2 = nullptr; int64_t out2_ts = 0;
   double* part = nullptr; int64_t slot0 = 0;
   bool serial = false;  // an inherently serial single-task step: split-K cluster kernel
+  double h2 = 0.0;      // E_PROP + out2: coarse-step advance from the same pre-activation
 };
 
 int family(const lmg_system& S, int B, int epi, const Fam& f, cudaStream_t st) {
@@ -580,6 +597,7 @@ int family(const lmg_system& S, int B, int epi, const Fam& f, cudaStream_t st) {
   a.out2 = f.out2; a.out2_ts = f.out2_ts;
   a.ldc = q;
   a.part = f.part; a.part_slot0 = f.slot0; a.part_ld = B;
+  a.h2 = f.h2;
   if (is_conv(S)) {
     const ConvGeom g = geom_of(S);
     a.M = B * g.HWp; a.N = g.C; a.K = 9 * g.Cp;
@@ -646,7 +664,7 @@ int seq_forward(const lmg_system& S, int B, const double* src, int mode, double*
 
 // F-sweep step i (1..c-1) of every block k: row kc+i from row kc+i-1
 int f_step(const lmg_system& S, int B, int c, double* U, const double* src, int mode, int i,
-           int k_first, cudaStream_t st) {
+           int k_first, cudaStream_t st, double* advH = nullptr) {
   const int64_t BQ = (int64_t)B * S.width;
   const int nb = S.num_layers / c;
   Fam f;
@@ -654,6 +672,10 @@ int f_step(const lmg_system& S, int B, int c, double* U, const double* src, int 
   f.x = U + (int64_t)(k_first * c + i - 1) * BQ; f.x_ts = c * BQ;
   f.s = src_fam(src, mode, BQ, k_first * c + i); f.s_ts = c * BQ;
   f.out = U + (int64_t)(k_first * c + i) * BQ; f.out_ts = c * BQ;
+  if (advH && i == 1) {  // rows kc: U[kc] + H*act(W_kc U[kc] + b_kc), H = c*h (coarse step)
+    f.out2 = advH; f.out2_ts = BQ;
+    f.h2 = S.step * c;
+  }
   return family(S, B, E_PROP, f, st);
 }
 
@@ -729,11 +751,18 @@ int local_fcf_a(const lmg_system& S, int B, int c, double* U, const double* src,
 // which only moves C rows.  With has_next, adv_out = U[(nb-1)c] + H F_H(U[(nb-1)c]) on the coarse
 // system: the next rank's first coarse-source row needs it (network.py:138).
 int local_fcf_b(const lmg_system& S, int B, int c, double* U, const double* src, int mode,
-                double* P, bool has_next, double* adv_out, cudaStream_t st) {
+                double* P, bool has_next, double* adv_out, cudaStream_t st,
+                double* advH = nullptr) {
   const int64_t BQ = (int64_t)B * S.width;
   const int nb = S.num_layers / c;
   const int K1 = nb - 1 + (has_next ? 1 : 0);
-  TRY(f_relax(S, B, c, U, src, mode, st));
+  // second F sweep; its first step also emits advH[k] = U[kc] + H F_H(U[kc]) for the coarse
+  // source (same weights W_kc and pre-activation as row kc+1, only the step differs)
+  for (int i = 1; i < c; ++i) TRY(f_step(S, B, c, U, src, mode, i, 0, st, advH));
+  if (has_next && adv_out && advH) {
+    TRY(copy_rows(adv_out, 0, advH + (int64_t)(nb - 1) * BQ, 0, 1, BQ, st));
+    adv_out = nullptr;  // done
+  }
   if (P) {
     Fam f;
     f.ntasks = K1; f.blk0 = c - 1; f.blk_step = c;
@@ -765,10 +794,24 @@ int fcf(const lmg_system& S, int B, int c, double* U, const double* src, int mod
 // (U[0] - adv_in) + (P[0] - U[0]) with the previous rank's adv.
 int local_coarse_source(const lmg_system& S, int B, int c, const double* U, const double* src,
                         int mode, const double* P, const double* adv_in, bool is_first, double* SH,
-                        double* V, cudaStream_t st) {
+                        double* V, cudaStream_t st, const double* advH = nullptr) {
   const int64_t BQ = (int64_t)B * S.width;
   const int nb = S.num_layers / c;
   const lmg_system Sc = coarsen(S, c);
+  if (advH) {  // S_H[n] = (U[nc] - advH[n-1]) + (P[n] - U[nc]); V[n] = U[nc]: elementwise
+    if (nb > 1)
+      TRY(launch(CLS_ELEM, 0.0, 40.0 * (nb - 1) * BQ, st, [&] {
+        k_coarse_from_adv<<<grid_for((int64_t)(nb - 1) * BQ), 256, 0, st>>>(
+            U + (int64_t)c * BQ, c * BQ, advH, P + BQ, SH + BQ, V ? V + BQ : nullptr, nb - 1, BQ);
+      }));
+    if (is_first)
+      return launch(CLS_ELEM, 0.0, 24.0 * BQ, st, [&] {
+        k_row0_coarse<<<grid_for(BQ), 256, 0, st>>>(U, src, SH, V, BQ);
+      });
+    return launch(CLS_ELEM, 0.0, 32.0 * BQ, st, [&] {
+      k_row0_coarse_halo<<<grid_for(BQ), 256, 0, st>>>(U, adv_in, P, SH, V, BQ);
+    });
+  }
   Fam f;
   f.ntasks = nb - 1; f.blk0 = 0; f.blk_step = 1;  // coarse block n-1 == fine block (n-1)c
   f.x = U; f.x_ts = c * BQ;
@@ -925,6 +968,7 @@ int levels_for(int n, int c, int threshold, std::vector<int>* sizes) {
 
 struct Workspace {
   std::vector<double*> P, SH, V;  // per relaxed level l: P[l]; per coarse level l+1: SH, V
+  std::vector<double*> advH;      // per relaxed level: U[kc] + H F_H(U[kc]) from the F sweep
   double* part = nullptr;         // residual partial-sum scratch
   double* block_part = nullptr;   // canonical per-block partials (N/c x B)
   double* Q = nullptr;            // finest level: propagate(U[kc]) rows from the last residual
@@ -945,10 +989,12 @@ int layout_ws(const lmg_system& fine, int nlevels, int c, int B, char* base, Wor
   ws->P.assign(nlevels, nullptr);
   ws->SH.assign(nlevels, nullptr);
   ws->V.assign(nlevels, nullptr);
+  ws->advH.assign(nlevels, nullptr);
   int n = fine.num_layers;
   for (int l = 0; l + 1 < nlevels; ++l) {
     int nb = n / c;
     ws->P[l] = take((size_t)(nb + 1) * BQ);
+    ws->advH[l] = take((size_t)nb * BQ);
     ws->SH[l + 1] = take((size_t)nb * BQ);
     ws->V[l + 1] = take((size_t)nb * BQ);
     n = nb;
@@ -989,12 +1035,13 @@ int cycle(const lmg_system& S, int nlevels, int l, int c, int B, double* U, cons
   const int nb = S.num_layers / c;
   double* P = ws.P[l];
   TRY(local_fcf_a(S, B, c, U, src, mode, true, false, (l == 0 && q_valid) ? ws.Q : nullptr, st));
-  TRY(local_fcf_b(S, B, c, U, src, mode, P, false, nullptr, st));
+  TRY(local_fcf_b(S, B, c, U, src, mode, P, false, nullptr, st, ws.advH[l]));
   const lmg_system Sc = coarsen(S, c);
   const bool coarsest = (l + 1 == nlevels - 1);
   double* SH = ws.SH[l + 1];
   double* V = ws.V[l + 1];
-  TRY(local_coarse_source(S, B, c, U, src, mode, P, nullptr, true, SH, coarsest ? nullptr : V, st));
+  TRY(local_coarse_source(S, B, c, U, src, mode, P, nullptr, true, SH, coarsest ? nullptr : V, st,
+                          ws.advH[l]));
   if (coarsest)
     TRY(seq_forward(Sc, B, SH, LMG_SRC_DENSE, V, st));
   else
@@ -1433,10 +1480,11 @@ int lmg_local_fcf_a(const lmg_system* sys, int B, int c, double* U, const double
 }
 
 int lmg_local_fcf_b(const lmg_system* sys, int B, int c, double* U, const double* src,
-                    int src_mode, double* P, int has_next, double* adv_out, void* stream) {
+                    int src_mode, double* P, int has_next, double* adv_out, double* advH,
+                    void* stream) {
   TRY(check_sys(sys, B));
   TRY(check_levels(*sys, 2, c));
-  return local_fcf_b(*sys, B, c, U, src, src_mode, P, has_next != 0, adv_out, S_(stream));
+  return local_fcf_b(*sys, B, c, U, src, src_mode, P, has_next != 0, adv_out, S_(stream), advH);
 }
 
 int lmg_halo_finish(const double* s0, const double* adv_in, double* out, int64_t len, void* stream) {
@@ -1449,11 +1497,12 @@ int lmg_halo_finish(const double* s0, const double* adv_in, double* out, int64_t
 int lmg_local_coarse_source(const lmg_system* sys, int B, int c, const double* U,
                             const double* src, int src_mode, const double* P,
                             const double* adv_in, int is_first, double* SH, double* V,
-                            void* stream) {
+                            const double* advH, void* stream) {
   TRY(check_sys(sys, B));
   TRY(check_levels(*sys, 2, c));
   if (!is_first && !adv_in) return fail(LMG_ERR_PROTOCOL, "non-first rank needs the previous rank's adv row");
-  return local_coarse_source(*sys, B, c, U, src, src_mode, P, adv_in, is_first != 0, SH, V, S_(stream));
+  return local_coarse_source(*sys, B, c, U, src, src_mode, P, adv_in, is_first != 0, SH, V,
+                             S_(stream), advH);
 }
 
 int lmg_local_correct(int n_blocks, int B, int q, int c, double* U, const double* V, void* stream) {

@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
           O[idx] = adv;
         } else if (epi == E_PROP) {
           O[idx] = __dadd_rn(S ? S[idx] : 0.0, adv);
+          if (O2) O2[idx] = __dadd_rn(X[idx], __dmul_rn(a.h2, v));
         } else if (epi == E_RESID) {
           const double prop = __dadd_rn(S ? S[idx] : 0.0, adv);
           const double r = __dadd_rn(prop, -Y[idx]);

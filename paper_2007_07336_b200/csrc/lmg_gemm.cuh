@@ -60,6 +60,7 @@ struct StepArgs {
   int ldc;
   double* part; int64_t part_slot0; int part_ld;
   int accum;  // E_PGRAD: add the gradient already in out2 (accumulate over batch slices)
+  double h2;  // E_PROP with out2: out2 = x + h2*act(pre) (the coarse step's advance, same pre)
 };
 
 __device__ __forceinline__ double act_fwd(int a, double v) {
@@ -284,6 +285,7 @@ __device__ __forceinline__ void epilogue(const StepArgs& a, const EpiPtrs& q, do
           q.O[idx] = adv;
         } else if (EPI == E_PROP) {
           q.O[idx] = __dadd_rn(q.S ? q.S[idx] : 0.0, adv);
+          if (q.O2) q.O2[idx] = __dadd_rn(q.X[idx], __dmul_rn(a.h2, v));
         } else if (EPI == E_RESID) {
           const double prop = __dadd_rn(q.S ? q.S[idx] : 0.0, adv);
           double r = __dadd_rn(prop, -q.Y[idx]);

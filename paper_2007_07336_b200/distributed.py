@@ -48,18 +48,18 @@ class CudaOps:
         _lib.call("lmg_local_fcf_a", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
                   int(is_first), int(has_next), self._p(Q), self._st())
 
-    def fcf_b(self, lv, U, S, smode, P, has_next, adv_out):
+    def fcf_b(self, lv, U, S, smode, P, has_next, adv_out, advH=None):
         _lib.call("lmg_local_fcf_b", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
-                  P.data_ptr(), int(has_next), self._p(adv_out), self._st())
+                  P.data_ptr(), int(has_next), self._p(adv_out), self._p(advH), self._st())
 
     def halo_finish(self, s0, adv, out):
         _lib.call("lmg_halo_finish", self._p(s0), adv.data_ptr(), out.data_ptr(), out.numel(),
                   self._st())
 
-    def coarse_source(self, lv, U, S, smode, P, adv_in, is_first, SH, V):
+    def coarse_source(self, lv, U, S, smode, P, adv_in, is_first, SH, V, advH=None):
         _lib.call("lmg_local_coarse_source", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
                   P.data_ptr(), self._p(adv_in), int(is_first), SH.data_ptr(), self._p(V),
-                  self._st())
+                  self._p(advH), self._st())
 
     def correct(self, lv, U, V):
         _lib.call("lmg_local_correct", lv.nb, lv.B, lv.q, lv.c, U.data_ptr(), V.data_ptr(), self._st())
@@ -156,12 +156,13 @@ class DistSolver:
         q = lv.q
         f64 = dict(dtype=t.float64, device=device)
         z = lambda *s: t.zeros(*s, **f64)  # noqa: E731
-        self.U, self.S, self.P = [], [], []
+        self.U, self.S, self.P, self.advH = [], [], [], []
         for l, lev in enumerate(self.levels):
             L = lev.L
             self.U.append(z(L + 1, B, q) if l > 0 else None)   # level 0 states are the caller's
             self.S.append(z(L + 1, B, q) if l > 0 else None)   # coarse sources, zero row L
             self.P.append(z(lev.nb + 2, B, q) if l < nlevels - 1 else None)  # + [P_out, adv_out]
+            self.advH.append(z(lev.nb, B, q) if l < nlevels - 1 else None)
         self.Q = z(lv.nb + 1, B, q)  # finest level: propagated rows kc+1 of the last residual
         self.q_valid = False
         self.recv1 = z(1, B, q)
@@ -251,14 +252,14 @@ class DistSolver:
         if not self.is_first:
             ops.halo_finish(None if S is None else S[0], self.recv1[0], U[0])
         adv_out = P[nb + 1] if self.has_next else None
-        ops.fcf_b(lev, U, S, smode, P, self.has_next, adv_out)
+        ops.fcf_b(lev, U, S, smode, P, self.has_next, adv_out, self.advH[l])
         self._exchange(P[nb : nb + 2] if self.has_next else None, self.recv2)
         if not self.is_first:
             ops.halo_finish(None if S is None else S[0], self.recv2[0], P[0])
         Vn, SHn = self.U[l + 1], self.S[l + 1]
         coarsest = l + 1 == self.nlevels - 1
         ops.coarse_source(lev, U, S, smode, P, None if self.is_first else self.recv2[1],
-                          self.is_first, SHn, None if coarsest else Vn)
+                          self.is_first, SHn, None if coarsest else Vn, self.advH[l])
         if coarsest:
             self._coarsest(l + 1, Vn, SHn)
         else:
