@@ -1,0 +1,55 @@
+"""CLI harness (cli.py mirror of the reference's cli.py:95-291): config handling and exit codes
+on CPU; the commands themselves on the GPU."""
+
+import json
+
+import pytest
+
+from paper_2007_07336_b200 import cli
+
+
+def _args(cmd, **kw):
+    ns = cli.build_parser().parse_args([cmd])
+    for k, v in kw.items():
+        setattr(ns, k, v)
+    return ns
+
+
+def test_defaults_and_flag_overrides():
+    cfg = cli.load_config("converge", _args("converge", depths="16,32", tol=1e-8))
+    assert cfg["depths"] == [16, 32] and cfg["tol"] == 1e-8 and cfg["width"] == 16
+
+
+def test_unknown_config_key_exits_2(tmp_path, capsys):
+    p = tmp_path / "c.json"
+    p.write_text(json.dumps({"depths": [8], "bogus": 1}))
+    assert cli.main(["converge", "--config", str(p)]) == cli.EXIT_CONFIG
+    assert "unknown keys" in capsys.readouterr().err
+
+
+def test_flag_not_applying_exits_2():
+    assert cli.main(["oracle-check", "--batches", "1,2"]) == cli.EXIT_CONFIG
+
+
+def test_bad_int_list_exits_2():
+    assert cli.main(["converge", "--depths", "8,x"]) == cli.EXIT_CONFIG
+
+
+def test_csv_layout(capsys):
+    cli.write_rows(None, ["a", "b"], [[1, 0.5]])
+    out = capsys.readouterr().out.splitlines()
+    assert out[0].startswith("# generated ") and out[1] == "a,b" and out[2] == "1,0.5"
+
+
+@pytest.mark.gpu
+def test_commands_on_gpu(tmp_path):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    out = tmp_path / "conv.csv"
+    assert cli.main(["converge", "--depths", "16,64", "--out", str(out)]) == cli.EXIT_OK
+    lines = out.read_text().splitlines()
+    assert lines[1] == "depth,cycle,residual_l2" and len(lines) > 4
+    assert cli.main(["oracle-check", "--depths", "16,64", "--seed", "0", "--out",
+                     str(tmp_path / "o.csv")]) == cli.EXIT_OK
+    assert cli.main(["scale", "--batches", "1,4", "--out", str(tmp_path / "s.csv")]) == cli.EXIT_OK
