@@ -36,9 +36,14 @@ class CudaOps:
 
     def __init__(self, device):
         self.device = device
+        self._stream = None
+
+    def bind_stream(self):
+        """Cache the current stream handle for the calls of one solve (host overhead)."""
+        self._stream = _lib.stream_handle(self.device)
 
     def _st(self):
-        return _lib.stream_handle(self.device)
+        return self._stream if self._stream is not None else _lib.stream_handle(self.device)
 
     @staticmethod
     def _p(t):
@@ -106,7 +111,11 @@ class LocalLevel:
         self.step = view.step
 
     def desc(self):
-        return self.view.desc(self.adjoint_D)
+        # the descriptor is static for a level (pointers into the parameter / D stacks): build once
+        d = getattr(self, "_desc", None)
+        if d is None:
+            d = self._desc = self.view.desc(self.adjoint_D)
+        return d
 
     def coarsen(self):
         return LocalLevel(self.view.coarsen(self.c), self.c, self.B, self.adjoint_D)
@@ -280,6 +289,8 @@ class DistSolver:
         t = self.t
         B = self.B
         L = self.levels[0].L
+        if hasattr(self.ops, "bind_stream"):
+            self.ops.bind_stream()
         if not use_initial:
             if self.is_first:
                 U0[:L].copy_(S0[0] if smode == _lib.SRC_DENSE else S0)
