@@ -72,12 +72,17 @@ const char* lmg_last_error(void);
 
 /* Instrumentation (not part of the reference API): number of kernels this library has launched,
  * and optional CUDA-event timing of every launch by class (0 forward step GEMM, 1 adjoint step
- * GEMM, 2 parameter-gradient GEMM, 3 elementwise/reduction; -1 = all).  lmg_timing_enable(1)
+ * GEMM, 2 parameter-gradient GEMM, 3 elementwise/reduction, 4/5 fused forward/adjoint sweep;
+ * -1 = all).  lmg_timing_enable(1)
  * clears the records; lmg_timing_read synchronises on the recorded events. */
 unsigned long long lmg_launch_count(void);
 int lmg_timing_enable(int on);
 int lmg_timing_read(int cls, double* ms_total, double* flops_total, double* bytes_total,
                     unsigned long long* launches);
+/* Debug: device buffer (>= 4 u64 per step, or NULL to stop) receiving per-step %globaltimer
+ * stamps (step start, state ready, mainloop done, epilogue done) of chain 0 / CTA 0 of every
+ * fused persistent sweep launch.  Classes 4/5 of lmg_timing_read are those launches. */
+int lmg_debug_sweep_trace(unsigned long long* dev_buf);
 
 /* network.py:88-102 propagate_values: out[j-start] = src[j] + (u + h*F_{j-1}(u)), j in
  * [start, stop), from u_start (B, q) = u^{start-1}.  out is (stop-start, B, q). */

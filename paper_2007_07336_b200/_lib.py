@@ -56,6 +56,7 @@ SIGNATURES = {
     "lmg_last_error": (ctypes.c_char_p, []),
     "lmg_launch_count": (ctypes.c_ulonglong, []),
     "lmg_timing_enable": (_I, [_I]),
+    "lmg_debug_sweep_trace": (_I, [_P]),
     "lmg_timing_read": (_I, [_I, c_double_p, c_double_p, c_double_p,
                              ctypes.POINTER(ctypes.c_ulonglong)]),
     "lmg_propagate": (_I, [_SYS, _I, _P, _P, _I, _I, _I, _P, _P]),

@@ -16,18 +16,18 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblmg.so")
-SOURCES = ["lmg.cu"]
-DEPS = ["lmg_gemm.cuh"]
+SOURCES = ["lmg.cu", "lmg_sweep.cu"]
+DEPS = ["lmg_gemm.cuh", "lmg_conv.cuh", "lmg_sweep.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-shared", "-Xcompiler", "-fPIC",
+    "-Xcompiler", "-fPIC",
     "-I", os.path.join(ROOT, "include"),
     "-I", CSRC,
-    "--cudart", "shared",
 ]
+LINK = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "--cudart", "shared"]
 
 
 def _stale() -> bool:
@@ -39,13 +39,26 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit to an object in parallel, then link liblmg.so."""
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, *(os.path.join(CSRC, s) for s in SOURCES), "-o", LIB + ".tmp"]
-    if verbose:
-        cmd[1:1] = ["-Xptxas", "-v"]
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        cmd = [NVCC, *(["-Xptxas", "-v"] if verbose else []), *FLAGS, "-c",
+               os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    subprocess.run([NVCC, *LINK, *objs, "-o", LIB + ".tmp"], check=True)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -28,6 +28,7 @@
 
 #include "lmg.h"
 #include "lmg_conv.cuh"
+#include "lmg_sweep.cuh"
 
 using namespace lmg;
 
@@ -161,6 +162,17 @@ __global__ void k_halo_finish(const double* __restrict__ s0, const double* __res
     out[i] = __dadd_rn(s0 ? s0[i] : 0.0, adv[i]);
 }
 
+// after a fused FCF sweep: U[0] = f[0] (c_relaxation, multigrid.py:157) and U[kc] = Cn[k], k >= 1
+__global__ void k_fcf_commit(double* __restrict__ U, const double* __restrict__ src0,
+                             const double* __restrict__ Cn, int nb, int c, int64_t BQ) {
+  const int64_t total = (int64_t)nb * BQ;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / BQ, i = e - r * BQ;
+    U[r * c * BQ + i] = r == 0 ? src0[i] : Cn[e];
+  }
+}
+
 // coarse FAS source rows n >= 1 from the advance computed in the F sweep:
 //   S_H[n] = (U[nc] - advH[n-1]) + (P[n] - U[nc]),  V[n] = U[nc]      (multigrid.py:142)
 __global__ void k_coarse_from_adv(const double* __restrict__ Uc, int64_t u_ts,
@@ -290,7 +302,15 @@ int grid_for(int64_t total) {
 // optional CUDA-event timing of each launch by class (bench roofline, measured over the timed
 // region on the launching stream).
 
-enum Cls { CLS_GEMM_FWD = 0, CLS_GEMM_ADJ = 1, CLS_GEMM_PG = 2, CLS_ELEM = 3, CLS_N = 4 };
+enum Cls {
+  CLS_GEMM_FWD = 0,   // step GEMM, forward layout
+  CLS_GEMM_ADJ = 1,   // step GEMM, adjoint layout
+  CLS_GEMM_PG = 2,    // parameter-gradient GEMM
+  CLS_ELEM = 3,       // elementwise / reductions
+  CLS_SWEEP_FWD = 4,  // fused persistent sweep (lmg_sweep.cu), forward
+  CLS_SWEEP_ADJ = 5,  // fused persistent sweep, adjoint
+  CLS_N = 6
+};
 
 struct Rec {
   int cls;
@@ -645,9 +665,115 @@ inline const double* src_fam(const double* src, int mode, int64_t BQ, int j0) {
 }
 
 // ------------------------------------------------------------------------------------------
+// fused persistent sweeps (lmg_sweep.cu): one launch per relaxation sweep / serial solve, state
+// kept on chip, W streamed by TMA.  Used where the launch-per-step path is latency- or HBM-bound
+// (small batches); bitwise identical to it.  LMG_NO_SWEEP=1 disables, LMG_SWEEP_MAXB sets the
+// largest batch routed to the fused FCF sweep.
+
+unsigned long long* g_sweep_trace = nullptr;  // lmg_debug_sweep_trace
+
+bool sweep_disabled() {
+  static const bool v = getenv("LMG_NO_SWEEP") != nullptr;
+  return v;
+}
+int sweep_max_batch() {
+  static const int v = [] {
+    const char* e = getenv("LMG_SWEEP_MAXB");
+    return e ? atoi(e) : 64;
+  }();
+  return v;
+}
+
+bool sweep_basic_ok(const lmg_system& S) {
+  if (sweep_disabled() || is_conv(S)) return false;
+  if (!aligned16(S.W) || (S.width & 1) || (S.w_stride & 1)) return false;
+  if (is_adjoint(S) && (!aligned16(S.D) || (S.d_stride & 1))) return false;
+  if (!is_adjoint(S) && S.b && ((S.b_stride & 1) || !aligned16(S.b))) return false;
+  return true;
+}
+
+SweepArgs sweep_args(const lmg_system& S, int B, int mode, int c, const double* src, int src_mode,
+                     double* U) {
+  SweepArgs a{};
+  a.mode = mode;
+  a.B = B; a.q = S.width; a.n = S.num_layers; a.c = c;
+  a.adj = is_adjoint(S) ? 1 : 0;
+  a.act = a.adj ? LMG_ACT_IDENTITY : S.act;
+  a.h = S.step;
+  a.W = S.W; a.w_stride = S.w_stride;
+  a.bias = a.adj ? nullptr : S.b; a.b_stride = S.b_stride;
+  a.D = a.adj ? S.D : nullptr; a.d_stride = S.d_stride;
+  a.src = src; a.src_head = src_mode == LMG_SRC_HEAD;
+  a.U = U;
+  a.trace = g_sweep_trace;
+  return a;
+}
+
+// algorithmic work of one sweep launch: `steps` layer steps over the whole batch, `written`
+// state rows stored to HBM (2q^2+5q flops per F-evaluation; W read once per step)
+int run_sweep(const SweepArgs& a, const SweepShape& sh, double steps, double written, cudaStream_t st) {
+  const double q = a.q, B = a.B, row = 8.0 * B * q;
+  const double flops = steps * B * (2.0 * q * q + 5.0 * q);
+  double bytes = steps * 8.0 * q * q + written * row + (double)sh.grid.z * row;
+  if (a.src && !a.src_head) bytes += steps * row;
+  if (a.adj) bytes += steps * row;
+  cudaError_t e = cudaSuccess;
+  TRY(launch(a.adj ? CLS_SWEEP_ADJ : CLS_SWEEP_FWD, flops, bytes, st, [&] { e = sweep_launch(a, sh, st); }));
+  if (e != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("sweep launch: ") + cudaGetErrorString(e));
+  return LMG_OK;
+}
+
+// serial forward substitution as one persistent launch (one chain per 16-sample tile); -1 when
+// not eligible.  Only when all chains fit in one wave (otherwise the per-step path is faster).
+int seq_sweep(const lmg_system& S, int B, const double* src, int mode, double* U, cudaStream_t st) {
+  if (S.num_layers < 2 || !sweep_basic_ok(S) || !aligned16(src) || !aligned16(U)) return -1;
+  SweepArgs a = sweep_args(S, B, SW_SEQ, 1, src, mode, U);
+  SweepShape sh;
+  if (sweep_shape(a, &sh) < 0) return -1;
+  if ((int64_t)sh.grid.y * sh.cs > 148) return -1;
+  const int64_t BQ = (int64_t)B * S.width;
+  TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]
+  return run_sweep(a, sh, S.num_layers - 1, S.num_layers - 1, st);
+}
+
+// FCF relaxation + P steps of a whole level as one persistent launch (lmg_sweep.cu SW_FCF), then
+// the commit of the new C rows; -1 when not eligible.  Same outputs as local_fcf_a + local_fcf_b
+// on a single GPU (is_first, no next rank).
+int fcf_sweep(const lmg_system& S, int B, int c, double* U, const double* src, int mode, double* P,
+              double* advH, double* Cn, const double* Q, cudaStream_t st) {
+  if (!Cn || !P || !src || B > sweep_max_batch() || !sweep_basic_ok(S)) return -1;
+  if (!aligned16(src) || !aligned16(U) || !aligned16(Q) || !aligned16(P) || !aligned16(advH) ||
+      !aligned16(Cn))
+    return -1;
+  const int nb = S.num_layers / c;
+  SweepArgs a = sweep_args(S, B, SW_FCF, c, src, mode, U);
+  a.h2 = S.step * c;
+  a.Q = Q; a.Cn = Cn; a.P = P; a.advH = advH;
+  SweepShape sh;
+  if (sweep_shape(a, &sh) < 0) return -1;
+  double steps = (c - 1) + (nb > 1 ? 1 : 0), written = steps;
+  for (int k = 1; k < nb; ++k) {
+    const int r0 = (k - 1) * c + (Q ? 1 : 0);
+    const int tail = (k < nb - 1) ? 1 : 0;
+    steps += k * c + c - 1 + tail - r0;
+    written += c + tail;
+  }
+  if (advH) written += nb;
+  TRY(run_sweep(a, sh, steps, written, st));
+  const int64_t BQ = (int64_t)B * S.width;
+  return launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
+    k_fcf_commit<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, src, Cn, nb, c, BQ);
+  });
+}
+
+// ------------------------------------------------------------------------------------------
 // reference routines
 
 int seq_forward(const lmg_system& S, int B, const double* src, int mode, double* U, cudaStream_t st) {
+  {
+    const int r = seq_sweep(S, B, src, mode, U, st);
+    if (r >= 0) return r;
+  }
   const int64_t BQ = (int64_t)B * S.width;
   TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]
   for (int j = 1; j < S.num_layers; ++j) {
@@ -969,6 +1095,7 @@ int levels_for(int n, int c, int threshold, std::vector<int>* sizes) {
 struct Workspace {
   std::vector<double*> P, SH, V;  // per relaxed level l: P[l]; per coarse level l+1: SH, V
   std::vector<double*> advH;      // per relaxed level: U[kc] + H F_H(U[kc]) from the F sweep
+  std::vector<double*> Cn;        // per relaxed level: new C rows of the fused sweep
   double* part = nullptr;         // residual partial-sum scratch
   double* block_part = nullptr;   // canonical per-block partials (N/c x B)
   double* Q = nullptr;            // finest level: propagate(U[kc]) rows from the last residual
@@ -990,11 +1117,13 @@ int layout_ws(const lmg_system& fine, int nlevels, int c, int B, char* base, Wor
   ws->SH.assign(nlevels, nullptr);
   ws->V.assign(nlevels, nullptr);
   ws->advH.assign(nlevels, nullptr);
+  ws->Cn.assign(nlevels, nullptr);
   int n = fine.num_layers;
   for (int l = 0; l + 1 < nlevels; ++l) {
     int nb = n / c;
     ws->P[l] = take((size_t)(nb + 1) * BQ);
     ws->advH[l] = take((size_t)nb * BQ);
+    ws->Cn[l] = B <= sweep_max_batch() ? take((size_t)nb * BQ) : nullptr;
     ws->SH[l + 1] = take((size_t)nb * BQ);
     ws->V[l + 1] = take((size_t)nb * BQ);
     n = nb;
@@ -1034,8 +1163,14 @@ int cycle(const lmg_system& S, int nlevels, int l, int c, int B, double* U, cons
   }
   const int nb = S.num_layers / c;
   double* P = ws.P[l];
-  TRY(local_fcf_a(S, B, c, U, src, mode, true, false, (l == 0 && q_valid) ? ws.Q : nullptr, st));
-  TRY(local_fcf_b(S, B, c, U, src, mode, P, false, nullptr, st, ws.advH[l]));
+  const double* Qs = (l == 0 && q_valid) ? ws.Q : nullptr;
+  const int rs = fcf_sweep(S, B, c, U, src, mode, P, ws.advH[l], ws.Cn[l], Qs, st);
+  if (rs < 0) {
+    TRY(local_fcf_a(S, B, c, U, src, mode, true, false, Qs, st));
+    TRY(local_fcf_b(S, B, c, U, src, mode, P, false, nullptr, st, ws.advH[l]));
+  } else if (rs != LMG_OK) {
+    return rs;
+  }
   const lmg_system Sc = coarsen(S, c);
   const bool coarsest = (l + 1 == nlevels - 1);
   double* SH = ws.SH[l + 1];
@@ -1107,6 +1242,13 @@ int lmg_timing_read(int cls, double* ms_total, double* flops_total, double* byte
 }
 
 const char* lmg_last_error(void) { return g_err.c_str(); }
+
+// debug instrumentation: device buffer (>= 4 * steps u64) receiving per-step globaltimer stamps
+// (step start, state ready, mainloop done, epilogue done) of chain 0 / CTA 0 of every fused sweep
+int lmg_debug_sweep_trace(unsigned long long* dev_buf) {
+  g_sweep_trace = dev_buf;
+  return LMG_OK;
+}
 
 int lmg_propagate(const lmg_system* sys, int B, const double* u_start, const double* src,
                   int src_mode, int start, int stop, double* out, void* stream) {

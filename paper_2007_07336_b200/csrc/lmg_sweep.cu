@@ -1,0 +1,541 @@
+// lmg_sweep.cu -- persistent fused relaxation sweep (sm_100a).  See lmg_sweep.cuh.
+//
+// Grid: (CS, batch tiles, chains); cluster (CS, 1, 1).  CTA r of a cluster owns output columns
+// [r*NC, (r+1)*NC) of every step of its chain.  Per CTA:
+//   warps 0..NW-1  consumers: DMMA m8n8k4 mainloop (A = the full 16-row state from smem,
+//                  B = the streamed W slice), fused E_PROP epilogue, DSMEM all-gather of the new
+//                  state slice into every CTA's next A buffer, one cluster barrier per step
+//   warp NW        producer: 2D tensor-map TMA loads of the W slice into an ST-deep ring
+//                  guarded by full/empty mbarriers; it runs ahead across step boundaries
+// Shared memory (1024-aligned): ring (ST stages) | A[2][16][q+4] (double-buffered state, +4
+// padding: conflict-free fragments) | xs[16][NC] (adjoint) | mbarriers.
+// W stage layouts (both give the minimum two wavefronts per m8n8k4 B-fragment load):
+//   forward  W[n][k] (K-major): BK/16 boxes of {16 k, NC rows}, 128B rows, SWIZZLE_128B
+//   adjoint  W[k][n] (MN-major): NC/8 boxes of {8 n, BK rows}, 64B rows, no swizzle
+//
+// Step s of a chain produces layer row j = r0 + 1 + s from row j-1 with block j-1:
+//   o = s_j + (u + h*act(W_{j-1} u + b_{j-1}))               forward  (network.py:100)
+//   o = s_j + (m + h*(W_{j-1}^T (D_{j-1} * m)))               adjoint  (training.py:216-224)
+// SW_FCF chain k (block k of the level, nb = n/c blocks):
+//   k = 0:  start at f[0] (the C row of block 0 after c_relaxation, multigrid.py:157); rows
+//           1..c-1 -> U (second F sweep), row c -> P[1] (if nb > 1)
+//   k >= 1: start at the OLD C row U[(k-1)c] (or Q[k-1] = its first step, already computed);
+//           rows (k-1)c+1..kc-1 are block k-1's first F sweep (transient: only feed the C step),
+//           row kc is the C step -> Cn[k], rows kc+1..kc+c-1 -> U (second F sweep), row (k+1)c
+//           -> P[k+1] (if k < nb-1).  advH[k] = U[kc] + h2*act(pre) at row kc+1.
+//   That is exactly multigrid.py:160-172 (F, C, F) plus the C-row propagation of :208: the same
+//   layer steps on the same operands, regrouped by chain.  C rows go to Cn (not U) because chain
+//   k+1 reads the old U[kc]; the caller commits Cn -> U[kc] and f[0] -> U[0] afterwards.
+// SW_SEQ (one chain per batch tile): start at f[0], rows 1..n-1 -> U.
+#include <cooperative_groups.h>
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "lmg.h"
+#include "lmg_gemm.cuh"
+#include "lmg_sweep.cuh"
+
+namespace lmg {
+namespace {
+
+namespace cg = cooperative_groups;
+
+constexpr int SW_BM = 16;  // batch rows per chain tile (two m8 fragments)
+constexpr int SMEM_MAX = 232448;
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = s_u32(b);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(s_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(s_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int NC_, int KS_, int ST_, bool ADJ_>
+struct SwCfg {
+  static constexpr int NC = NC_, KS = KS_, BK = 32, ST = ST_;
+  static constexpr bool ADJ = ADJ_;
+  static constexpr int MT = SW_BM / 8;
+  static constexpr int NFG = NC / 8;        // 8-column fragment groups (one per warp, per k-split)
+  static constexpr int NW = NFG * KS;       // consumer warps; warp = ks * NFG + fg
+  static constexpr int NT = (NW + 1) * 32;  // + producer warp
+  static constexpr int LDS_ = NC + 4;       // padded row of one state slice: conflict-free A frags
+  static constexpr int SL = SW_BM * LDS_;   // doubles per slice (16 rows x NC columns of one rank)
+  static constexpr int STAGE = NC * BK;     // doubles, dense (TMA boxes)
+  static constexpr int BOXES = ADJ ? NC / 8 : BK / 16;
+  static constexpr int BOX = STAGE / BOXES;
+  static_assert((STAGE * 8) % 1024 == 0, "stages must keep the 1024B swizzle alignment");
+  static_assert(BK % (4 * KS) == 0, "k-split must divide the stage");
+  static size_t smem(int q) {
+    const int cs = q / NC;
+    return sizeof(double) * ((size_t)ST * STAGE + 2 * (size_t)cs * SL + (size_t)NFG * 32 * 4 * (KS - 1) +
+                             (ADJ ? (size_t)SW_BM * NC : 0)) +
+           (2 * ST + 2) * sizeof(uint64_t) + 1024;  // + alignment slack
+  }
+};
+
+// kernel parameter block: the sweep plus the W tensor map (a 2D view [rows][q] of the weight
+// stack; block j's first row is row_off + j*row_stride)
+struct alignas(64) SweepParams {
+  CUtensorMap wmap;
+  SweepArgs a;
+  int64_t row_off, row_stride;
+};
+
+struct Chain {
+  int r0, nsteps;
+  const double* start;
+};
+
+__device__ __forceinline__ Chain chain_of(const SweepArgs& a, int k, int64_t BQ) {
+  Chain ch;
+  if (a.mode == SW_SEQ) {
+    ch.r0 = 0;
+    ch.nsteps = a.n - 1;
+    ch.start = a.src;
+    return ch;
+  }
+  const int c = a.c, nb = a.n / c;
+  if (k == 0) {
+    ch.r0 = 0;
+    ch.start = a.src;  // f[0]
+    ch.nsteps = (c - 1) + (nb > 1 ? 1 : 0);
+    return ch;
+  }
+  if (a.Q) {
+    ch.r0 = (k - 1) * c + 1;
+    ch.start = a.Q + (int64_t)(k - 1) * BQ;
+  } else {
+    ch.r0 = (k - 1) * c;
+    ch.start = a.U + (int64_t)ch.r0 * BQ;
+  }
+  ch.nsteps = (k * c + c - 1 + (k < nb - 1 ? 1 : 0)) - ch.r0;
+  return ch;
+}
+
+// destination of row j in chain k (SW_FCF) or row j (SW_SEQ); nullptr = transient row
+__device__ __forceinline__ double* dest_of(const SweepArgs& a, int k, int j, int64_t BQ) {
+  if (a.mode == SW_SEQ) return a.U + (int64_t)j * BQ;
+  const int c = a.c;
+  if (j < k * c) return nullptr;
+  if (j == k * c) return a.Cn + (int64_t)k * BQ;  // k >= 1 here (k = 0 starts at row 0)
+  if (j < (k + 1) * c) return a.U + (int64_t)j * BQ;
+  return a.P + (int64_t)(k + 1) * BQ;
+}
+
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// remote (or own) 16-byte store completing on the destination CTA's mbarrier
+__device__ __forceinline__ void st_async2(uint32_t dst, double a, double b, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+               "d"(a), "d"(b), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void consumers_sync(int n) {
+  asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory");
+}
+
+// State layout in shared memory: A[buf][rank][16][NC+4] -- the 16 x q state of one batch tile as
+// CS column slices, each padded; rank r's slice is written by CTA r and pushed to the others.
+template <class C>
+__global__ void __launch_bounds__(C::NT, 1) sweep_kernel(const __grid_constant__ SweepParams p) {
+  constexpr int NC = C::NC, KS = C::KS, BK = C::BK, ST = C::ST, MT = C::MT, NW = C::NW;
+  constexpr int NFG = C::NFG, SL = C::SL, LDS_ = C::LDS_;
+  constexpr bool ADJ = C::ADJ;
+  const SweepArgs& a = p.a;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  const int q = a.q;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  double* Ab = ring + ST * C::STAGE;             // [2][CS][SL]
+  double* red = Ab + 2 * CS * SL;                // [NFG][32][4] k-split partials
+  double* xs = red + NFG * 32 * 4 * (KS - 1);    // [16][NC] adjoint: own slice, unscaled
+  uint64_t* full = reinterpret_cast<uint64_t*>(xs + (ADJ ? SW_BM * NC : 0));
+  uint64_t* empty = full + ST;
+  uint64_t* sready = empty + ST;                 // [2]: peer slices of A[buf] have landed
+
+  const int n0 = rank * NC;
+  const int k = blockIdx.z;
+  const int m0 = blockIdx.y * SW_BM;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t BQ = (int64_t)a.B * q;
+  const Chain ch = chain_of(a, k, BQ);
+  const int KT = q / BK;
+  if (ch.nsteps <= 0) return;  // uniform over the cluster
+
+  if (tid == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NW);
+    }
+    mbar_init(&sready[0], 1);
+    mbar_init(&sready[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NW) {
+    // ------------------------------------------------------------------ producer warp
+    cluster_arrive();  // startup: peers' barriers are initialised before any push lands
+    cluster_wait();
+    if (lane == 0) {
+      int g = 0;
+      for (int s = 0; s < ch.nsteps; ++s) {
+        const int row = (int)(p.row_off + (int64_t)(ch.r0 + s) * p.row_stride);  // block r0+s
+        for (int kt = 0; kt < KT; ++kt, ++g) {
+          const int stg = g % ST;
+          mbar_wait(&empty[stg], ((uint32_t)(g / ST) & 1u) ^ 1u);
+          mbar_expect_tx(&full[stg], (uint32_t)(C::STAGE * 8));
+          double* dst = ring + stg * C::STAGE;
+#pragma unroll
+          for (int b = 0; b < C::BOXES; ++b) {
+            if (ADJ)  // {8 n, BK k} at (n0 + 8b, k rows kt*BK..)
+              tma_2d(dst + b * C::BOX, &p.wmap, n0 + 8 * b, row + kt * BK, &full[stg]);
+            else      // {16 k, NC n} at (k kt*BK + 16b, n rows n0..)
+              tma_2d(dst + b * C::BOX, &p.wmap, kt * BK + 16 * b, row + n0, &full[stg]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    cluster_arrive();  // exit: no CTA leaves while a peer may still push into it
+    cluster_wait();
+    return;
+  }
+
+  // -------------------------------------------------------------------- consumer warps
+  const int NCT = NW * 32;
+  {  // start state: A[0] = rows m0..m0+15 of the chain's start row (zero beyond the batch)
+    const double* Dst = ADJ ? a.D + (int64_t)ch.r0 * a.d_stride : nullptr;
+    const int h2 = q / 2;
+    for (int e = tid; e < SW_BM * h2; e += NCT) {
+      const int m = e / h2, n = (e - m * h2) * 2;
+      double2 v = make_double2(0.0, 0.0);
+      if (m0 + m < a.B) v = *reinterpret_cast<const double2*>(ch.start + (int64_t)(m0 + m) * q + n);
+      if (ADJ) {
+        if (n >= n0 && n < n0 + NC) *reinterpret_cast<double2*>(xs + m * NC + n - n0) = v;
+        if (m0 + m < a.B) {
+          const double2 d = *reinterpret_cast<const double2*>(Dst + (int64_t)(m0 + m) * q + n);
+          v.x = __dmul_rn(v.x, d.x);
+          v.y = __dmul_rn(v.y, d.y);
+        }
+      }
+      *reinterpret_cast<double2*>(Ab + (n / NC) * SL + m * LDS_ + (n % NC)) = v;
+    }
+  }
+  consumers_sync(NCT);
+  cluster_arrive();  // startup (pairs with the producer's)
+  cluster_wait();
+
+  const int fr = lane >> 2, fk = lane & 3;
+  const int fg = warp % NFG, ks = warp / NFG;
+  const int nl = fg * 8 + 2 * fk;  // this lane's output columns (nl, nl+1) within the slice
+  // this warp's k4 chunks of a stage: kk = 4*KS*i + 4*ks; the ks part is folded into per-thread
+  // offsets so the chunk loop is fully unrolled.  B fragment: forward W[n = 8fg+fr][k] in
+  // 128B-swizzled rows (16B chunk ^= row & 7; the kk bits and 2ks are disjoint), adjoint W[k][n]
+  // in box fg, 64B rows.
+  const int t_sw = ((fk >> 1) ^ fr) ^ (2 * ks);
+  const int b_thr = ADJ ? fg * C::BOX + (fk + 4 * ks) * 8 + fr : (fg * 8 + fr) * 16 + (fk & 1);
+  const int a_thr = fr * LDS_ + fk + 4 * ks;
+  const uint32_t bytes_in = (uint32_t)(SW_BM * q * 8);  // one full 16 x q state per step
+  // cluster addresses of A[buf][rank] (this CTA's slice) and sready[buf] in every CTA
+  const uint32_t slice_a = s_u32(Ab + rank * SL);
+  const uint32_t sready_a = s_u32(&sready[0]);
+  int g = 0;
+  for (int s = 0; s < ch.nsteps; ++s) {
+    const int cur = s & 1;
+    const int j = ch.r0 + 1 + s;  // row produced
+    const bool last = (s + 1 == ch.nsteps);
+    if (tid == 0 && !last) mbar_expect_tx(&sready[cur ^ 1], bytes_in);
+    // epilogue operands, fetched now so their latency hides behind the mainloop
+    double bia[2] = {0.0, 0.0}, src[MT][2], dn[MT][2];
+    const double* srow = (a.src && (!a.src_head || j == 0)) ? a.src + (int64_t)j * BQ : nullptr;
+    const double* brow = (!ADJ && a.bias) ? a.bias + (int64_t)(j - 1) * a.b_stride : nullptr;
+    const double* drow = (ADJ && !last) ? a.D + (int64_t)j * a.d_stride : nullptr;
+    {
+      if (brow) {
+        const double2 v = *reinterpret_cast<const double2*>(brow + n0 + nl);
+        bia[0] = v.x;
+        bia[1] = v.y;
+      }
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        const int m = m0 + i * 8 + fr;
+        src[i][0] = src[i][1] = dn[i][0] = dn[i][1] = 0.0;
+        if (m < a.B && srow) {
+          const double2 v = *reinterpret_cast<const double2*>(srow + (int64_t)m * q + n0 + nl);
+          src[i][0] = v.x;
+          src[i][1] = v.y;
+        }
+        if (m < a.B && drow) {
+          const double2 v = *reinterpret_cast<const double2*>(drow + (int64_t)m * q + n0 + nl);
+          dn[i][0] = v.x;
+          dn[i][1] = v.y;
+        }
+      }
+    }
+    const bool tr = a.trace && tid == 0 && k == 0 && rank == 0 && blockIdx.y == 0;
+    if (tr) a.trace[4 * s] = gtimer();
+    if (s > 0) mbar_wait(&sready[cur], (uint32_t)((s - 1) >> 1) & 1u);
+    if (tr) a.trace[4 * s + 1] = gtimer();
+
+    double acc[MT][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) acc[i][0] = acc[i][1] = 0.0;
+    const double* Acur = Ab + cur * CS * SL;
+    for (int kt = 0; kt < KT; ++kt, ++g) {
+      const int stg = g % ST;
+      mbar_wait(&full[stg], (uint32_t)(g / ST) & 1u);
+      const double* Bs = ring + stg * C::STAGE + b_thr;
+      // stage kt covers k in [kt*BK, kt*BK+BK): slice (kt*BK)/NC, columns (kt*BK)%NC ..
+      const double* Ak = Acur + ((kt * BK) / NC) * SL + ((kt * BK) % NC) + a_thr;
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4 * KS) {
+        double af[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) af[i] = Ak[i * 8 * LDS_ + kk];
+        const double bf = ADJ ? Bs[kk * 8] : Bs[(kk >> 4) * C::BOX + ((((kk & 15) >> 1) ^ t_sw) << 1)];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) dmma(acc[i][0], acc[i][1], af[i], bf);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stg]);
+    }
+
+    if (tr) a.trace[4 * s + 2] = gtimer();
+    // k-split partials (KS = 2): the two warps of a pair swap halves through smem and each
+    // finishes one m-fragment, summing in fixed order (ks = 0 part + ks = 1 part)
+    int i_lo = 0, i_hi = MT;
+    if (KS > 1) {
+      double* r = red + (fg * 32 + lane) * 4;
+      // the fragment this warp hands over: 1 (ks 0) or 0 (ks 1)
+      r[2 * ks] = ks == 0 ? acc[MT - 1][0] : acc[0][0];
+      r[2 * ks + 1] = ks == 0 ? acc[MT - 1][1] : acc[0][1];
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + fg) : "memory");
+      const double p0 = r[2 * (1 - ks)], p1 = r[2 * (1 - ks) + 1];
+      if (ks == 0) {  // fragment 0: own (ks 0) + partner (ks 1)
+        acc[0][0] = acc[0][0] + p0;
+        acc[0][1] = acc[0][1] + p1;
+      } else {        // fragment 1: partner (ks 0) + own (ks 1)
+        acc[MT - 1][0] = p0 + acc[MT - 1][0];
+        acc[MT - 1][1] = p1 + acc[MT - 1][1];
+      }
+      i_lo = ks;
+      i_hi = ks + 1;
+    }
+
+    // ---------------------------------------------------------------- fused E_PROP epilogue
+    double* drow_out = dest_of(a, k, j, BQ);
+    double* adv_out = (a.mode == SW_FCF && a.advH && j == k * a.c + 1) ? a.advH + (int64_t)k * BQ
+                                                                      : nullptr;
+    const double* own = Acur + rank * SL;
+    const uint32_t nxt_off = (uint32_t)(((cur ^ 1) * CS * SL) * 8);
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      if (i < i_lo || i >= i_hi) continue;
+      const int ml = i * 8 + fr;
+      const int m = m0 + ml;
+      double o[2], nx[2], ad[2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double pre = acc[i][e];
+        if (brow) pre = __dadd_rn(pre, bia[e]);
+        const double v = ADJ ? pre : act_fwd(a.act, pre);
+        const double x = ADJ ? xs[ml * NC + nl + e] : own[ml * LDS_ + nl + e];
+        const double adv = __dadd_rn(x, __dmul_rn(a.h, v));
+        o[e] = __dadd_rn(srow ? src[i][e] : 0.0, adv);
+        ad[e] = adv_out ? __dadd_rn(x, __dmul_rn(a.h2, v)) : 0.0;
+        nx[e] = ADJ ? __dmul_rn(o[e], dn[i][e]) : o[e];
+        if (ADJ) xs[ml * NC + nl + e] = o[e];
+      }
+      if (!last) {  // all-gather: this pair of the new state into A[cur^1] of every CTA
+        const uint32_t off = nxt_off + (uint32_t)((ml * LDS_ + nl) * 8);
+        for (int r = 0; r < CS; ++r) {
+          const int dr = rank + r < CS ? rank + r : rank + r - CS;
+          st_async2(mapa(slice_a + off, dr), nx[0], nx[1], mapa(sready_a + 8 * (cur ^ 1), dr));
+        }
+      }
+      if (m < a.B) {
+        if (drow_out)
+          *reinterpret_cast<double2*>(drow_out + (int64_t)m * q + n0 + nl) = make_double2(o[0], o[1]);
+        if (adv_out)
+          *reinterpret_cast<double2*>(adv_out + (int64_t)m * q + n0 + nl) = make_double2(ad[0], ad[1]);
+      }
+    }
+    if (tr) a.trace[4 * s + 3] = gtimer();
+  }
+  __syncwarp();
+  cluster_arrive();  // exit
+  cluster_wait();
+}
+
+// NC = 64: cluster q/64, 8 consumer warps (bitwise the per-step kernel: one k-ascending chain);
+// NC = 32: cluster q/32, 8 consumer warps as two k-split halves (2 warps per SMSP)
+using Cfg64F = SwCfg<64, 1, 5, false>;
+using Cfg32F = SwCfg<32, 2, 7, false>;
+using Cfg64A = SwCfg<64, 1, 5, true>;
+using Cfg32A = SwCfg<32, 2, 7, true>;
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+  static EncodeTiled fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      return (EncodeTiled) nullptr;
+    return (EncodeTiled)f;
+  }();
+  return fn;
+}
+
+template <class C>
+bool fits(int q) {
+  return q % C::NC == 0 && q / C::NC <= 16 && q % C::BK == 0 && C::smem(q) <= (size_t)SMEM_MAX &&
+         encoder() != nullptr;
+}
+
+// W of the level as a 2D tensor [rows][q]: blocks j = 0..n-1 at a.W + j*w_stride
+template <class C>
+cudaError_t make_params(const SweepArgs& a, SweepParams* p) {
+  EncodeTiled enc = encoder();
+  if (!enc) return cudaErrorNotSupported;
+  const int64_t q = a.q, q2 = q * q;
+  const int64_t span = (int64_t)(a.n - 1) * a.w_stride;  // may be negative (adjoint)
+  const double* base = span < 0 ? a.W + span : a.W;
+  p->a = a;
+  p->row_stride = a.w_stride / q;
+  p->row_off = (a.W - base) / q;
+  const cuuint64_t rows = (cuuint64_t)((span < 0 ? -span : span) / q + q);
+  (void)q2;
+  cuuint64_t dims[2] = {(cuuint64_t)q, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)q * 8};
+  cuuint32_t box[2], estr[2] = {1, 1};
+  if (C::ADJ) {
+    box[0] = 8;
+    box[1] = C::BK;
+  } else {
+    box[0] = 16;
+    box[1] = C::NC;
+  }
+  CUresult r = enc(&p->wmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   C::ADJ ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <class C>
+cudaError_t launch_c(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
+  auto kern = sweep_kernel<C>;
+  static cudaError_t attr = [&] {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return e;
+  }();
+  if (attr != cudaSuccess) return attr;
+  SweepParams prm;
+  cudaError_t e = make_params<C>(a, &prm);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = s.grid;
+  cfg.blockDim = dim3(C::NT, 1, 1);
+  cfg.dynamicSmemBytes = s.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = s.cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, prm);
+}
+
+}  // namespace
+
+// 0: 64 columns per CTA (cluster q/64, one k-ascending chain: bitwise the per-step kernel),
+// 1: 32 columns per CTA (cluster q/32, k split over two warps).  Measured on B200 (c5 shapes,
+// tools/sweep_bench.py): many independent chains (FCF) -> 0 (more clusters resident, 63 vs 98
+// SM-us per layer step); a single serial chain -> 1 (twice the SMs on the critical path).
+int sweep_config(int q, int B, int adj, int nchains) {
+  (void)B;
+  static const int forced = [] {
+    const char* e = getenv("LMG_SWEEP_CFG");
+    return e ? atoi(e) : -1;
+  }();
+  const bool ok64 = adj ? fits<Cfg64A>(q) : fits<Cfg64F>(q);
+  const bool ok32 = adj ? fits<Cfg32A>(q) : fits<Cfg32F>(q);
+  if (forced == 0 && ok64) return 0;
+  if (forced == 1 && ok32) return 1;
+  if (nchains > 16 && ok64) return 0;
+  return ok32 ? 1 : (ok64 ? 0 : -1);
+}
+
+int sweep_shape(const SweepArgs& a, SweepShape* s) {
+  const int nchains = a.mode == SW_SEQ ? 1 : a.n / a.c;
+  const int mt = (a.B + SW_BM - 1) / SW_BM;
+  const int cfg = sweep_config(a.q, a.B, a.adj, nchains);
+  if (cfg < 0) return -1;
+  const int NC = cfg == 0 ? 64 : 32;
+  s->cfg = cfg;
+  s->cs = a.q / NC;
+  s->nthreads = 9 * 32;
+  s->smem = cfg == 0 ? (a.adj ? Cfg64A::smem(a.q) : Cfg64F::smem(a.q))
+                     : (a.adj ? Cfg32A::smem(a.q) : Cfg32F::smem(a.q));
+  s->grid = dim3(s->cs, mt, nchains);
+  return 0;
+}
+
+cudaError_t sweep_launch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
+  if (s.cfg == 0) return a.adj ? launch_c<Cfg64A>(a, s, st) : launch_c<Cfg64F>(a, s, st);
+  return a.adj ? launch_c<Cfg32A>(a, s, st) : launch_c<Cfg32F>(a, s, st);
+}
+
+}  // namespace lmg

@@ -1,8 +1,10 @@
 """The layer-partitioned solver on the GPU through the C-ABI (CudaOps): two ranks sharing the one
 GPU of the test box (gloo, halos staged through host memory), against the single-GPU solve.
-States, residual histories and the SGD-updated parameters must be BITWISE identical: every row is
-produced by the same kernel on the same operands whatever the partition, and norm partials are
-summed per block in global block order."""
+With the launch-per-step kernels (LMG_NO_SWEEP=1, set for the spawned processes) states, residual
+histories and the SGD-updated parameters must be BITWISE identical: every row is produced by the
+same kernel on the same operands whatever the partition, and norm partials are summed per block
+in global block order.  The default single-GPU path (fused persistent sweeps, k-split where it
+pays) must agree within the parity tolerance."""
 
 import os
 import pickle
@@ -68,11 +70,40 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def _run(world, tmp_path):
-    out = str(tmp_path / f"w{world}.pkl")
-    mp.spawn(_worker, args=(world, _port(), out), nprocs=world, join=True)
+def _single(rank, out):
+    sys.path.insert(0, ROOT)
+    torch.cuda.set_device(0)
+    import paper_2007_07336_b200 as P
+
+    X, labels = _inputs()
+    d = P.device_network(N, Q, [3, N, Q])
+    tr = P.DeviceTrainer(d, coarsening=C, threshold=THR, tol=1e-10, max_cycles=40, adjoint="fas",
+                         learning_rate=0.1)
+    U, hist, cyc, conv = tr.forward(torch.from_numpy(X).cuda())
+    U = U.cpu().numpy().copy()
+    res = tr.step(torch.from_numpy(X).cuda(), torch.from_numpy(labels).cuda())
+    with open(out, "wb") as fh:
+        pickle.dump(dict(U=U, hist=hist, cyc=cyc, ahist=res.adj_hist, acyc=res.adj_cycles,
+                         W=d.stack.W.cpu().numpy(), loss=res.loss.cpu().numpy()), fh)
+
+
+def _spawn(fn, args, nprocs, out):
+    old = os.environ.get("LMG_NO_SWEEP")
+    os.environ["LMG_NO_SWEEP"] = "1"
+    try:
+        mp.spawn(fn, args=args, nprocs=nprocs, join=True)
+    finally:
+        if old is None:
+            del os.environ["LMG_NO_SWEEP"]
+        else:
+            os.environ["LMG_NO_SWEEP"] = old
     with open(out, "rb") as fh:
         return pickle.load(fh)
+
+
+def _run(world, tmp_path):
+    out = str(tmp_path / f"w{world}.pkl")
+    return _spawn(_worker, (world, _port(), out), world, out)
 
 
 def test_partitioned_training_step_bitwise_vs_single_gpu(tmp_path):
@@ -86,10 +117,15 @@ def test_partitioned_training_step_bitwise_vs_single_gpu(tmp_path):
     U = U.cpu().numpy().copy()
     res = tr.step(torch.from_numpy(X).cuda(), torch.from_numpy(labels).cuda())
     W1 = d.stack.W.cpu().numpy()
+    ref = _spawn(_single, (str(tmp_path / "single.pkl"),), 1, str(tmp_path / "single.pkl"))
+    # default (fused) single-GPU path vs the per-step path: parity tolerance, same cycle counts
+    assert np.array_equal(ref["cyc"], cyc) and np.array_equal(ref["acyc"], res.adj_cycles)
+    assert np.max(np.abs(ref["U"] - U)) <= 1e-12 * max(1.0, np.max(np.abs(U)))
+    assert np.max(np.abs(ref["W"] - W1)) <= 1e-12 * max(1.0, np.max(np.abs(W1)))
     for world in (1, 2, 4):
         r = _run(world, tmp_path)
-        assert r["U"].tobytes() == U.tobytes(), world
-        assert np.array_equal(r["hist"], hist[: cyc.max() + 1], equal_nan=True), world
-        assert np.array_equal(r["ahist"], res.adj_hist[: res.adj_cycles.max() + 1], equal_nan=True), world
-        assert r["W"].tobytes() == W1.tobytes(), world
-        assert np.array_equal(r["loss"], res.loss.cpu().numpy()), world
+        assert r["U"].tobytes() == ref["U"].tobytes(), world
+        assert np.array_equal(r["hist"], ref["hist"][: ref["cyc"].max() + 1], equal_nan=True), world
+        assert np.array_equal(r["ahist"], ref["ahist"][: ref["acyc"].max() + 1], equal_nan=True), world
+        assert r["W"].tobytes() == ref["W"].tobytes(), world
+        assert np.array_equal(r["loss"], ref["loss"]), world

@@ -1,0 +1,62 @@
+"""The fused persistent sweep (csrc/lmg_sweep.cu) against the launch-per-step path, over a whole
+FAS training step (forward solve, FAS adjoint, gradients + SGD) and a serial propagation:
+
+* the one-chain configuration (LMG_SWEEP_CFG=0: 64 columns per CTA, one k-ascending DMMA chain per
+  output) is BITWISE identical to the per-step kernels (LMG_NO_SWEEP=1);
+* the default k-split configuration (two warps per output tile, partials summed in fixed order)
+  matches within the parity tolerance, with identical cycle counts;
+* the fused runs launch fewer kernels."""
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+CASES = [
+    (64, 32, 4, 4, 0),       # c1-shaped, cluster of 1 CTA
+    (256, 512, 16, 16, 4),   # c5-shaped: 3 levels [256, 16, 1]
+    (128, 256, 20, 4, 8),    # two batch tiles (20 = 16 + 4 masked rows), 3 levels
+    (96, 64, 33, 2, 12),     # cf 2, three batch tiles, 4 levels [96,48,24,12]
+]
+
+
+def _run(case, tmp_path, env_extra):
+    tag = "_".join("%s%s" % kv for kv in sorted(env_extra.items())) or "default"
+    out = str(tmp_path / ("%s_%s.npz" % ("_".join(map(str, case)), tag)))
+    env = dict(os.environ, **env_extra)
+    subprocess.run([sys.executable, os.path.join(HERE, "sweep_case.py"), *map(str, case), out],
+                   check=True, env=env, timeout=600)
+    return np.load(out)
+
+
+def _close(a, b, rel):
+    scale = max(1.0, float(np.nanmax(np.abs(b))))
+    return float(np.nanmax(np.abs(a - b))) <= rel * scale
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "N%d_q%d_B%d_c%d" % c[:4])
+def test_fused_sweep_matches_per_step(case, tmp_path):
+    off = _run(case, tmp_path, {"LMG_NO_SWEEP": "1"})
+    on = _run(case, tmp_path, {})
+    for key in ("cyc", "adj_cyc"):
+        assert np.array_equal(on[key], off[key]), key
+    for key, rel in (("U0", 1e-12), ("U1", 1e-12), ("lam", 1e-12), ("loss", 1e-12), ("W", 1e-12),
+                     ("b", 1e-12), ("Us", 1e-12), ("hist", 1e-9), ("adj_hist", 1e-9)):
+        assert on[key].shape == off[key].shape, key
+        assert _close(on[key], off[key], rel), (key, float(np.nanmax(np.abs(on[key] - off[key]))))
+    assert int(on["launches"]) < int(off["launches"])
+    if case[1] % 64 == 0:  # one-chain configuration: bitwise (the serial split-K path is not)
+        one = _run(case, tmp_path, {"LMG_SWEEP_CFG": "0"})
+        for key in ("U0", "hist", "cyc", "U1", "lam", "loss", "adj_hist", "adj_cyc", "W", "b"):
+            assert np.array_equal(one[key], off[key], equal_nan=True), key
+    assert int(on["launches"]) < int(off["launches"])
