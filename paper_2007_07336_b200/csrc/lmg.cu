@@ -730,6 +730,9 @@ int seq_sweep(const lmg_system& S, int B, const double* src, int mode, double* U
   SweepArgs a = sweep_args(S, B, SW_SEQ, 1, src, mode, U);
   SweepShape sh;
   if (sweep_shape(a, &sh) < 0) return -1;
+  if ((int64_t)sh.grid.y * sh.cs > 148 && sh.cfg == 1) {  // wider CTAs: half the cluster size
+    if (sweep_shape(a, &sh, 0) < 0) return -1;
+  }
   if ((int64_t)sh.grid.y * sh.cs > 148) return -1;
   const int64_t BQ = (int64_t)B * S.width;
   TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]
@@ -751,6 +754,11 @@ int fcf_sweep(const lmg_system& S, int B, int c, double* U, const double* src, i
   a.Q = Q; a.Cn = Cn; a.P = P; a.advH = advH;
   SweepShape sh;
   if (sweep_shape(a, &sh) < 0) return -1;
+  // latency-bound levels only: when every chain of the level is resident at once (one wave of
+  // clusters).  With more chains than that the per-step launches keep all SMs streaming W and
+  // measured faster (c5 fine level: 64 chains x 8 CTAs).  LMG_SWEEP_ALL=1 lifts the limit.
+  static const bool all = getenv("LMG_SWEEP_ALL") != nullptr;
+  if (!all && (int64_t)sh.grid.x * sh.grid.y * sh.grid.z > 148) return -1;
   double steps = (c - 1) + (nb > 1 ? 1 : 0), written = steps;
   for (int k = 1; k < nb; ++k) {
     const int r0 = (k - 1) * c + (Q ? 1 : 0);

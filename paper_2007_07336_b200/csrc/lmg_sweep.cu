@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(C::NT, 1) sweep_kernel(const __grid_constant__
   // cluster addresses of A[buf][rank] (this CTA's slice) and sready[buf] in every CTA
   const uint32_t slice_a = s_u32(Ab + rank * SL);
   const uint32_t sready_a = s_u32(&sready[0]);
-  int g = 0;
+  int g = 0, prev_stg = -1;
   for (int s = 0; s < ch.nsteps; ++s) {
     const int cur = s & 1;
     const int j = ch.r0 + 1 + s;  // row produced
@@ -340,8 +340,14 @@ __global__ void __launch_bounds__(C::NT, 1) sweep_kernel(const __grid_constant__
 #pragma unroll
         for (int i = 0; i < MT; ++i) dmma(acc[i][0], acc[i][1], af[i], bf);
       }
+      // Release the PREVIOUS stage's slot, not this one: the slot's next fill is an async-proxy
+      // (TMA) write, and ptxas hoists the arrive above this stage's DMMAs, i.e. possibly before
+      // this stage's LDS have returned (observed: stale W boxes under load).  The previous
+      // stage's LDS results were consumed by DMMAs issued before this stage's, so its reads are
+      // complete.  (A fence.proxy.async per stage also works but costs ~1 us per step.)
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stg]);
+      if (lane == 0 && prev_stg >= 0) mbar_arrive(&empty[prev_stg]);
+      prev_stg = stg;
     }
 
     if (tr) a.trace[4 * s + 2] = gtimer();
@@ -518,10 +524,12 @@ int sweep_config(int q, int B, int adj, int nchains) {
   return ok32 ? 1 : (ok64 ? 0 : -1);
 }
 
-int sweep_shape(const SweepArgs& a, SweepShape* s) {
+int sweep_shape(const SweepArgs& a, SweepShape* s, int forced_cfg) {
   const int nchains = a.mode == SW_SEQ ? 1 : a.n / a.c;
   const int mt = (a.B + SW_BM - 1) / SW_BM;
-  const int cfg = sweep_config(a.q, a.B, a.adj, nchains);
+  int cfg = sweep_config(a.q, a.B, a.adj, nchains);
+  if (forced_cfg == 0 && (a.adj ? fits<Cfg64A>(a.q) : fits<Cfg64F>(a.q))) cfg = 0;
+  if (forced_cfg == 1 && (a.adj ? fits<Cfg32A>(a.q) : fits<Cfg32F>(a.q))) cfg = 1;
   if (cfg < 0) return -1;
   const int NC = cfg == 0 ? 64 : 32;
   s->cfg = cfg;

@@ -27,6 +27,7 @@ CASES = [
     (256, 512, 16, 16, 4),   # c5-shaped: 3 levels [256, 16, 1]
     (128, 256, 20, 4, 8),    # two batch tiles (20 = 16 + 4 masked rows), 3 levels
     (96, 64, 33, 2, 12),     # cf 2, three batch tiles, 4 levels [96,48,24,12]
+    (64, 512, 160, 4, 16),   # B > 64: per-step FCF, serial coarsest solve on 10 batch tiles
 ]
 
 
@@ -56,7 +57,8 @@ def test_fused_sweep_matches_per_step(case, tmp_path):
         assert _close(on[key], off[key], rel), (key, float(np.nanmax(np.abs(on[key] - off[key]))))
     assert int(on["launches"]) < int(off["launches"])
     if case[1] % 64 == 0:  # one-chain configuration: bitwise (the serial split-K path is not)
-        one = _run(case, tmp_path, {"LMG_SWEEP_CFG": "0"})
+        one = _run(case, tmp_path, {"LMG_SWEEP_CFG": "0", "LMG_NO_SPLITK": "1"})
+        off = _run(case, tmp_path, {"LMG_NO_SWEEP": "1", "LMG_NO_SPLITK": "1"})  # one chain too
         for key in ("U0", "hist", "cyc", "U1", "lam", "loss", "adj_hist", "adj_cyc", "W", "b"):
             assert np.array_equal(one[key], off[key], equal_nan=True), key
     assert int(on["launches"]) < int(off["launches"])

@@ -36,8 +36,14 @@ def main():
         return solve_device(view, tr.nlevels, c, f0, U, src_mode=_lib.SRC_HEAD, use_initial=False,
                             tol=1e-9, max_cycles=50)
 
-    names = {0: "gemm_fwd", 1: "gemm_adj", 3: "elem", 4: "sweep_fwd", 5: "sweep_adj"}
-    for label, fn in (("serial", serial), ("fas", fas)):
+    names = {0: "gemm_fwd", 1: "gemm_adj", 2: "gemm_pg", 3: "elem", 4: "sweep_fwd", 5: "sweep_adj"}
+    labels = torch.from_numpy(np.arange(B) % 10).cuda()
+
+    def step():
+        r = tr.step(X, labels)
+        return (None, r.fwd_cycles) if r.adj_cycles is None else (None, np.concatenate([r.fwd_cycles, r.adj_cycles]))
+
+    for label, fn in (("serial", serial), ("fas", fas), ("train_step", step)):
         for _ in range(2):
             fn()
         torch.cuda.synchronize()
@@ -64,8 +70,10 @@ if __name__ == "__main__":
     main()
 
 
-def trace(N=1024, q=512, B=16):
+def trace(N=None, q=512, B=None):
     """Per-step phase times of one serial fused sweep (lmg_debug_sweep_trace)."""
+    N = N or int(os.environ.get("LMG_TRACE_N", 1024))
+    B = B or int(os.environ.get("LMG_TRACE_B", 16))
     import ctypes
 
     import torch
