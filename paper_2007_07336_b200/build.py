@@ -16,8 +16,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblmg.so")
-SOURCES = ["lmg.cu", "lmg_sweep.cu"]
-DEPS = ["lmg_gemm.cuh", "lmg_conv.cuh", "lmg_sweep.cuh"]
+SOURCES = ["lmg.cu", "lmg_sweep.cu", "lmg_tgemm.cu"]
+DEPS = ["lmg_gemm.cuh", "lmg_conv.cuh", "lmg_sweep.cuh", "lmg_async.cuh", "lmg_tgemm.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -29,6 +29,7 @@
 #include "lmg.h"
 #include "lmg_conv.cuh"
 #include "lmg_sweep.cuh"
+#include "lmg_tgemm.cuh"
 
 using namespace lmg;
 
@@ -400,7 +401,10 @@ int n_tiles(int N) { return (N + TSmall::BN - 1) / TSmall::BN; }
 
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-enum TileSel { SEL_AUTO = 0, SEL_SMALL = 1, SEL_WIDE = 2, SEL_TINY = 3 };
+enum TileSel { SEL_AUTO = 0, SEL_SMALL = 1, SEL_WIDE = 2, SEL_TINY = 3, SEL_X1 = 4, SEL_X2 = 5 };
+// experimental shapes (LMG_TILE=x1|x2, fully tiled only), for tools/gemm_bench.py sweeps
+using TX1 = Tile<32, 32, 32, 2, 2, 3>;  // BK 32: half the k-tile barriers
+using TX2 = Tile<64, 32, 16, 4, 2, 4>;  // 8 warps of 16x16, W tile reused by 64 batch rows
 
 int tile_override() {
   static int v = [] {
@@ -408,6 +412,8 @@ int tile_override() {
     if (e && !strcmp(e, "small")) return (int)SEL_SMALL;
     if (e && !strcmp(e, "wide")) return (int)SEL_WIDE;
     if (e && !strcmp(e, "tiny")) return (int)SEL_TINY;
+    if (e && !strcmp(e, "x1")) return (int)SEL_X1;
+    if (e && !strcmp(e, "x2")) return (int)SEL_X2;
     return (int)SEL_AUTO;
   }();
   return v;
@@ -435,6 +441,8 @@ int launch_layout(const StepArgs& a, bool v2, cudaStream_t st) {
     return a.M % BM == 0 && a.N % BN == 0 && a.K % BK == 0 && !getenv("LMG_NO_FULL");
   };
   const int sel = choose_tile<AK, BKM, ASC>(a);
+  if (sel == SEL_X1 && full(TX1::BM, TX1::BN, TX1::BK)) return launch_cfg<TX1, AK, BKM, ASC, 2, true>(a, st);
+  if (sel == SEL_X2 && full(TX2::BM, TX2::BN, TX2::BK)) return launch_cfg<TX2, AK, BKM, ASC, 2, true>(a, st);
   if (sel == SEL_TINY) {
     if (full(TTiny::BM, TTiny::BN, TTiny::BK)) return launch_cfg<TTiny, AK, BKM, ASC, 2, true>(a, st);
     return launch_cfg<TTiny, AK, BKM, ASC, 2>(a, st);
@@ -502,6 +510,18 @@ int launch_step(Layout L, const StepArgs& a, cudaStream_t st) {
   if (L == L_FWD) v2 = v2 && (a.K % 2 == 0);
   if (L == L_ADJ) v2 = v2 && (a.K % 2 == 0) && (a.N % 2 == 0);
   if (L == L_PG) v2 = v2 && (a.M % 2 == 0) && (a.N % 2 == 0);
+  if (L != L_PG && v2 && tgemm_eligible(a, L == L_ADJ)) {
+    // big-batch steps: the warp-specialised TMA kernel (lmg_tgemm.cu), bitwise the same math
+    const int cls = L == L_FWD ? CLS_GEMM_FWD : CLS_GEMM_ADJ;
+    const double flops = (double)a.ntasks * ((double)a.M * a.N * (2.0 * a.K + 5.0));
+    const double bytes = 8.0 * a.ntasks * ((double)a.N * a.K + (double)a.M * a.K + 2.0 * a.M * a.N);
+    bool launched = false;
+    cudaError_t e = cudaSuccess;
+    TRY(launch(cls, flops, bytes, st, [&] { e = tgemm_launch(a, L == L_ADJ, st, &launched); }));
+    if (e != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("tgemm: ") + cudaGetErrorString(e));
+    if (launched) return LMG_OK;
+    g_launches--;  // nothing was launched: fall through to step_gemm
+  }
   switch (L) {
     case L_FWD: return launch_layout<true, true, false>(a, v2, st);
     case L_ADJ: return launch_layout<true, false, true>(a, v2, st);
@@ -730,9 +750,8 @@ int seq_sweep(const lmg_system& S, int B, const double* src, int mode, double* U
   SweepArgs a = sweep_args(S, B, SW_SEQ, 1, src, mode, U);
   SweepShape sh;
   if (sweep_shape(a, &sh) < 0) return -1;
-  if ((int64_t)sh.grid.y * sh.cs > 148 && sh.cfg == 1) {  // wider CTAs: half the cluster size
-    if (sweep_shape(a, &sh, 0) < 0) return -1;
-  }
+  // one wave of 16-CTA clusters only: beyond that (B > 144) the split-K per-step path measured
+  // faster (B = 256, 64 steps: 12.4 vs 18.7 us per step with 8-CTA clusters in two waves)
   if ((int64_t)sh.grid.y * sh.cs > 148) return -1;
   const int64_t BQ = (int64_t)B * S.width;
   TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]

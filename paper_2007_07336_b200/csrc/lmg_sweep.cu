@@ -35,6 +35,7 @@
 #include "lmg.h"
 #include "lmg_gemm.cuh"
 #include "lmg_sweep.cuh"
+#include "lmg_async.cuh"
 
 namespace lmg {
 namespace {
@@ -43,45 +44,6 @@ namespace cg = cooperative_groups;
 
 constexpr int SW_BM = 16;  // batch rows per chain tile (two m8 fragments)
 constexpr int SMEM_MAX = 232448;
-
-__device__ __forceinline__ uint32_t s_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, int cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  const uint32_t a = s_u32(b);
-  uint32_t ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                       uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(s_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(s_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void cluster_arrive() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void cluster_wait() {
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 
 template <int NC_, int KS_, int ST_, bool ADJ_>
 struct SwCfg {
@@ -94,7 +56,8 @@ struct SwCfg {
   static constexpr int LDS_ = NC + 4;       // padded row of one state slice: conflict-free A frags
   static constexpr int SL = SW_BM * LDS_;   // doubles per slice (16 rows x NC columns of one rank)
   static constexpr int STAGE = NC * BK;     // doubles, dense (TMA boxes)
-  static constexpr int BOXES = ADJ ? NC / 8 : BK / 16;
+  static constexpr int BOXES = ADJ ? NC / 8 : BK / 16;  // fewer, wider boxes: TMA issue-bound
+                                                       // (32B-row boxes measured slower here)
   static constexpr int BOX = STAGE / BOXES;
   static_assert((STAGE * 8) % 1024 == 0, "stages must keep the 1024B swizzle alignment");
   static_assert(BK % (4 * KS) == 0, "k-split must divide the stage");
@@ -155,11 +118,6 @@ __device__ __forceinline__ double* dest_of(const SweepArgs& a, int k, int j, int
   return a.P + (int64_t)(k + 1) * BQ;
 }
 
-__device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
 // remote (or own) 16-byte store completing on the destination CTA's mbarrier
 __device__ __forceinline__ void st_async2(uint32_t dst, double a, double b, uint32_t bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
