@@ -403,8 +403,8 @@ bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr
 
 enum TileSel { SEL_AUTO = 0, SEL_SMALL = 1, SEL_WIDE = 2, SEL_TINY = 3, SEL_X1 = 4, SEL_X2 = 5 };
 // experimental shapes (LMG_TILE=x1|x2, fully tiled only), for tools/gemm_bench.py sweeps
-using TX1 = Tile<32, 32, 32, 2, 2, 3>;  // BK 32: half the k-tile barriers
-using TX2 = Tile<64, 32, 16, 4, 2, 4>;  // 8 warps of 16x16, W tile reused by 64 batch rows
+using TX1 = Tile<16, 64, 16, 1, 4, 4>;  // small batch: 4 warps of 16x16, 64 columns
+using TX2 = Tile<16, 32, 32, 1, 2, 3>;  // small batch: BK 32, half the k-tile barriers
 
 int tile_override() {
   static int v = [] {

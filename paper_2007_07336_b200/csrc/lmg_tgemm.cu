@@ -29,20 +29,29 @@
 namespace lmg {
 namespace {
 
-constexpr int TBM = 64, TBN = 64, TBK = 16;
+constexpr int TBK = 16;
 
-template <bool ADJ>
+// BM x BN output tile per CTA, WM x WN DMMA warps (warp tile (BM/WM) x (BN/WN)), ST ring stages,
+// MINB CTAs per SM.  Big: 64 x 64, 8 warps of 32 x 16, persistent (2/SM).  Small batch (M <= 16,
+// HBM/latency-bound): 16 x 32, 4 warps of 16 x 8, 8 CTAs/SM so one wave covers a c5 sweep step.
+template <bool ADJ_, int BM_, int BN_, int WM_, int WN_, int ST_, int MINB_>
 struct TG {
-  static constexpr int A_SZ = TBM * TBK;  // doubles per operand slab (8 KB)
-  static constexpr int B_SZ = TBN * TBK;
-  static constexpr int D_SZ = ADJ ? TBM * TBK : 0;
+  static constexpr bool ADJ = ADJ_;
+  static constexpr int BM = BM_, BN = BN_, WM = WM_, WN = WN_, ST = ST_, MINB = MINB_;
+  static constexpr int MT = BM / WM / 8, NTF = BN / WN / 8;
+  static constexpr int A_SZ = BM * TBK;  // doubles per operand slab
+  static constexpr int B_SZ = BN * TBK;
+  static constexpr int D_SZ = ADJ ? BM * TBK : 0;
   static constexpr int STAGE = A_SZ + B_SZ + D_SZ;
-  static constexpr int ST = ADJ ? 4 : 6;
-  static constexpr int NW = 8;  // DMMA warps: 2 (m) x 4 (n) of 32 x 16
+  static constexpr int NW = WM * WN;
   static constexpr int NT = (NW + 1) * 32;
   static constexpr size_t SMEM = (size_t)STAGE * 8 * ST + 2 * ST * 8 + 1024;
   static_assert((A_SZ * 8) % 128 == 0 && (STAGE * 8) % 128 == 0, "TMA destinations 128B-aligned");
 };
+using TBig = TG<false, 64, 64, 2, 4, 6, 2>;
+using TBigA = TG<true, 64, 64, 2, 4, 4, 2>;
+using TSm = TG<false, 16, 32, 1, 4, 4, 8>;
+using TSmA = TG<true, 16, 32, 1, 4, 3, 8>;
 
 struct alignas(64) TgParams {
   CUtensorMap amap, bmap, dmap;
@@ -53,19 +62,21 @@ struct alignas(64) TgParams {
   int mtiles, ntiles, ntiles_total;
 };
 
-// K-major slab of four {4 k, 64 rows} boxes: element (row, k) at box k/4
-__device__ __forceinline__ int kmaj(int row, int k) { return (k >> 2) * 256 + row * 4 + (k & 3); }
+// K-major slab of four {4 k, ROWS rows} boxes: element (row, k) at box k/4
+template <int ROWS>
+__device__ __forceinline__ int kmaj(int row, int k) { return (k >> 2) * (ROWS * 4) + row * 4 + (k & 3); }
 
-template <bool ADJ, int EPI>
-__device__ __forceinline__ void run_epi(const StepArgs& a, const EpiPtrs& q, double (&acc)[4][2][2],
+template <int EPI, int MT, int NTF>
+__device__ __forceinline__ void run_epi(const StepArgs& a, const EpiPtrs& q, double (&acc)[MT][NTF][2],
                                         int mrow0, int ncol0) {
-  double rowsq[4];
+  double rowsq[MT];
   epilogue<EPI>(a, q, acc, mrow0, ncol0, rowsq);
 }
 
-template <bool ADJ>
-__global__ void __launch_bounds__(TG<ADJ>::NT, 2) tgemm_kernel(const __grid_constant__ TgParams p) {
-  using C = TG<ADJ>;
+template <class C>
+__global__ void __launch_bounds__(C::NT, C::MINB) tgemm_kernel(const __grid_constant__ TgParams p) {
+  constexpr bool ADJ = C::ADJ;
+  constexpr int BM = C::BM, BN = C::BN, MT = C::MT, NTF = C::NTF;
   const StepArgs& a = p.a;
   extern __shared__ __align__(1024) unsigned char smraw[];
   const uint32_t pad = (1024u - (s_u32(smraw) & 1023u)) & 1023u;
@@ -92,27 +103,27 @@ __global__ void __launch_bounds__(TG<ADJ>::NT, 2) tgemm_kernel(const __grid_cons
       for (int tile = blockIdx.x; tile < p.ntiles_total; tile += gridDim.x) {
         const int t = tile / per_task, r = tile - t * per_task;
         const int mt = r / p.ntiles, nt = r - mt * p.ntiles;
-        const int arow = (int)(p.a_row0 + (int64_t)t * p.a_rowts) + mt * TBM;
+        const int arow = (int)(p.a_row0 + (int64_t)t * p.a_rowts) + mt * BM;
         const int brow = (int)(p.b_row0 + (int64_t)t * p.b_rowts);
-        const int drow = ADJ ? (int)(p.d_row0 + (int64_t)t * p.d_rowts) + mt * TBM : 0;
+        const int drow = ADJ ? (int)(p.d_row0 + (int64_t)t * p.d_rowts) + mt * BM : 0;
         for (int kt = 0; kt < KT; ++kt, ++g) {
           const int stg = g % C::ST;
           mbar_wait(&empty[stg], ((uint32_t)(g / C::ST) & 1u) ^ 1u);
           mbar_expect_tx(&full[stg], (uint32_t)(C::STAGE * 8));
           double* dst = ring + stg * C::STAGE;
 #pragma unroll
-          for (int b = 0; b < TBK / 4; ++b) tma_2d(dst + b * 256, &p.amap, kt * TBK + 4 * b, arow, &full[stg]);
+          for (int b = 0; b < TBK / 4; ++b) tma_2d(dst + b * BM * 4, &p.amap, kt * TBK + 4 * b, arow, &full[stg]);
           if (ADJ) {
 #pragma unroll
-            for (int b = 0; b < TBN / 4; ++b)  // {4 n, 16 k}: W[k][n]
-              tma_2d(dst + C::A_SZ + b * 64, &p.bmap, nt * TBN + 4 * b, brow + kt * TBK, &full[stg]);
+            for (int b = 0; b < BN / 4; ++b)  // {4 n, 16 k}: W[k][n]
+              tma_2d(dst + C::A_SZ + b * 64, &p.bmap, nt * BN + 4 * b, brow + kt * TBK, &full[stg]);
 #pragma unroll
             for (int b = 0; b < TBK / 4; ++b)
-              tma_2d(dst + C::A_SZ + C::B_SZ + b * 256, &p.dmap, kt * TBK + 4 * b, drow, &full[stg]);
+              tma_2d(dst + C::A_SZ + C::B_SZ + b * BM * 4, &p.dmap, kt * TBK + 4 * b, drow, &full[stg]);
           } else {
 #pragma unroll
             for (int b = 0; b < TBK / 4; ++b)
-              tma_2d(dst + C::A_SZ + b * 256, &p.bmap, kt * TBK + 4 * b, brow + nt * TBN, &full[stg]);
+              tma_2d(dst + C::A_SZ + b * BN * 4, &p.bmap, kt * TBK + 4 * b, brow + nt * BN, &full[stg]);
           }
         }
       }
@@ -122,16 +133,17 @@ __global__ void __launch_bounds__(TG<ADJ>::NT, 2) tgemm_kernel(const __grid_cons
 
   // ------------------------------------------------------------------------ DMMA warps
   const int fr = lane >> 2, fk = lane & 3;
-  const int wm = warp >> 2, wn = warp & 3;  // 32-row x 16-column sub-tile
+  const int wm = warp / C::WN, wn = warp % C::WN;  // (BM/WM) x (BN/WN) sub-tile
+  constexpr int WTM = BM / C::WM, WTN = BN / C::WN;
   int g = 0, prev = -1;
   for (int tile = blockIdx.x; tile < p.ntiles_total; tile += gridDim.x) {
     const int t = tile / per_task, r = tile - t * per_task;
     const int mt = r / p.ntiles, nt = r - mt * p.ntiles;
-    double acc[4][2][2];
+    double acc[MT][NTF][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < MT; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < NTF; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     for (int kt = 0; kt < KT; ++kt, ++g) {
       const int stg = g % C::ST;
@@ -141,21 +153,21 @@ __global__ void __launch_bounds__(TG<ADJ>::NT, 2) tgemm_kernel(const __grid_cons
       const double* Ds = Bs + C::B_SZ;
 #pragma unroll
       for (int kk = 0; kk < TBK; kk += 4) {
-        double af[4], bf[2];
+        double af[MT], bf[NTF];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int o = kmaj(wm * 32 + i * 8 + fr, kk + fk);
+        for (int i = 0; i < MT; ++i) {
+          const int o = kmaj<BM>(wm * WTM + i * 8 + fr, kk + fk);
           af[i] = As[o];
           if (ADJ) af[i] = __dmul_rn(af[i], Ds[o]);
         }
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
-          bf[j] = ADJ ? Bs[((wn * 16 + j * 8 + fr) >> 2) * 64 + (kk + fk) * 4 + (fr & 3)]
-                      : Bs[kmaj(wn * 16 + j * 8 + fr, kk + fk)];
+        for (int j = 0; j < NTF; ++j)
+          bf[j] = ADJ ? Bs[((wn * WTN + j * 8 + fr) >> 2) * 64 + (kk + fk) * 4 + (fr & 3)]
+                      : Bs[kmaj<BN>(wn * WTN + j * 8 + fr, kk + fk)];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < MT; ++i)
 #pragma unroll
-          for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int j = 0; j < NTF; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
       }
       __syncwarp();
       if (lane == 0 && prev >= 0) mbar_arrive(&empty[prev]);
@@ -171,15 +183,15 @@ __global__ void __launch_bounds__(TG<ADJ>::NT, 2) tgemm_kernel(const __grid_cons
     q.P = a.p ? a.p + (int64_t)t * a.p_ts : nullptr;
     q.O = a.out ? a.out + (int64_t)t * a.out_ts : nullptr;
     q.O2 = a.out2 ? a.out2 + (int64_t)t * a.out2_ts : nullptr;
-    const int mrow0 = mt * TBM + wm * 32 + fr, ncol0 = nt * TBN + wn * 16 + 2 * fk;
+    const int mrow0 = mt * BM + wm * WTM + fr, ncol0 = nt * BN + wn * WTN + 2 * fk;
     switch (a.epi) {
-      case E_PROP: run_epi<ADJ, E_PROP>(a, q, acc, mrow0, ncol0); break;
-      case E_COARSE: run_epi<ADJ, E_COARSE>(a, q, acc, mrow0, ncol0); break;
-      case E_COARSE_R: run_epi<ADJ, E_COARSE_R>(a, q, acc, mrow0, ncol0); break;
-      case E_PROPOP: run_epi<ADJ, E_PROPOP>(a, q, acc, mrow0, ncol0); break;
-      case E_DERIV: run_epi<ADJ, E_DERIV>(a, q, acc, mrow0, ncol0); break;
-      case E_APPLY: run_epi<ADJ, E_APPLY>(a, q, acc, mrow0, ncol0); break;
-      default: run_epi<ADJ, E_ADV>(a, q, acc, mrow0, ncol0); break;
+      case E_PROP: run_epi<E_PROP>(a, q, acc, mrow0, ncol0); break;
+      case E_COARSE: run_epi<E_COARSE>(a, q, acc, mrow0, ncol0); break;
+      case E_COARSE_R: run_epi<E_COARSE_R>(a, q, acc, mrow0, ncol0); break;
+      case E_PROPOP: run_epi<E_PROPOP>(a, q, acc, mrow0, ncol0); break;
+      case E_DERIV: run_epi<E_DERIV>(a, q, acc, mrow0, ncol0); break;
+      case E_APPLY: run_epi<E_APPLY>(a, q, acc, mrow0, ncol0); break;
+      default: run_epi<E_ADV>(a, q, acc, mrow0, ncol0); break;
     }
   }
 }
@@ -222,10 +234,9 @@ bool make_map(CUtensorMap* map, int64_t* row0, int64_t* rowts, const double* ptr
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <bool ADJ>
+template <class C>
 cudaError_t launch_t(TgParams& prm, cudaStream_t st) {
-  using C = TG<ADJ>;
-  auto kern = tgemm_kernel<ADJ>;
+  auto kern = tgemm_kernel<C>;
   static cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)C::SMEM);
   if (attr != cudaSuccess) return attr;
@@ -235,53 +246,66 @@ cudaError_t launch_t(TgParams& prm, cudaStream_t st) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     return n;
   }();
-  const int grid = prm.ntiles_total < 2 * sms ? prm.ntiles_total : 2 * sms;
+  const int slots = C::MINB * sms;
+  const int grid = prm.ntiles_total < slots ? prm.ntiles_total : slots;
   kern<<<grid, C::NT, C::SMEM, st>>>(prm);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-// Routing (measured on B200, tools/gemm_bench.py, 256 tasks x 256x512x512): the adjoint layout
-// runs 27.4 TF/s here vs 26.3 in step_gemm; the forward 26.9 vs 28.0 (step_gemm's 5 CTAs/SM hide
-// the FP64 tanh epilogue better than 2 persistent CTAs), so forward steps stay on step_gemm unless
-// LMG_TGEMM=all.
-int tgemm_eligible(const StepArgs& a, bool adj) {
+// Routing (measured on B200): big batches (M % 64 == 0; tools/gemm_bench.py, 256 tasks x
+// 256x512x512) -- the adjoint layout runs 27.4 TF/s here vs 26.3 in step_gemm, the forward 26.9
+// vs 28.0 (step_gemm's 5 CTAs/SM hide the FP64 tanh epilogue better than 2 persistent CTAs), so
+// big forward steps stay on step_gemm unless LMG_TGEMM=all.  The 16 x 32 small-batch variant
+// (M = 16, the c5 regime) is bitwise too but measured slower than step_gemm's 16-row tiles
+// (c5 fine-level step 3.40 vs 3.76 TB/s), so it only runs with LMG_TGEMM=small.
+namespace {
+int tile_kind(const StepArgs& a, bool adj) {  // 0: none, 1: big, 2: small
   static const bool off = getenv("LMG_NO_TGEMM") != nullptr;
-  static const bool all = [] {
+  static const int mode = [] {  // 0 default, 1 all, 2 small
     const char* e = getenv("LMG_TGEMM");
-    return e && !strcmp(e, "all");
+    return !e ? 0 : !strcmp(e, "all") ? 1 : !strcmp(e, "small") ? 2 : 0;
   }();
-  if (off || !encoder() || (!adj && !all)) return 0;
-  if (a.epi == E_RESID || a.epi == E_PGRAD) return 0;
-  if (a.M % TBM || a.N % TBN || a.K % TBK || a.M <= 0 || a.ntasks <= 0) return 0;
-  if ((int64_t)a.ntasks * (a.M / TBM) * (a.N / TBN) >= ((int64_t)1 << 31)) return 0;
+  const bool all = mode == 1;
+  if (off || !encoder()) return 0;
+  if (a.epi == E_RESID || a.epi == E_PGRAD || a.M <= 0 || a.ntasks <= 0 || a.K % TBK) return 0;
   if (adj && !a.Ds) return 0;
-  return 1;
+  if (mode == 2 && a.M == 16 && a.N % 32 == 0) return 2;
+  if (a.M % 64 == 0 && a.N % 64 == 0 && (adj || all)) return 1;
+  return 0;
 }
+}  // namespace
+
+int tgemm_eligible(const StepArgs& a, bool adj) { return tile_kind(a, adj) != 0; }
 
 cudaError_t tgemm_launch(const StepArgs& a, bool adj, cudaStream_t st, bool* launched) {
   *launched = false;
+  const int kind = tile_kind(a, adj);
+  if (!kind) return cudaSuccess;
+  const int BM = kind == 1 ? 64 : 16, BN = kind == 1 ? 64 : 32;
+  if ((int64_t)a.ntasks * (a.M / BM) * (a.N / BN) >= ((int64_t)1 << 31)) return cudaSuccess;
   TgParams prm;
   prm.a = a;
-  prm.mtiles = a.M / TBM;
-  prm.ntiles = a.N / TBN;
+  prm.mtiles = a.M / BM;
+  prm.ntiles = a.N / BN;
   prm.ntiles_total = a.ntasks * prm.mtiles * prm.ntiles;
   // A: rows m of task t (K-major, lda); W: forward rows n (K-major, ldb), adjoint rows k (ldb)
-  if (!make_map(&prm.amap, &prm.a_row0, &prm.a_rowts, a.A, a.A_ts, a.ntasks, a.M, a.lda, 4, TBM, false))
+  if (!make_map(&prm.amap, &prm.a_row0, &prm.a_rowts, a.A, a.A_ts, a.ntasks, a.M, a.lda, 4, BM, false))
     return cudaSuccess;
   if (!make_map(&prm.bmap, &prm.b_row0, &prm.b_rowts, a.Bm, a.B_ts, a.ntasks, adj ? a.K : a.N, a.ldb,
-                4, adj ? TBK : TBN, false))
+                4, adj ? TBK : BN, false))
     return cudaSuccess;
   if (adj && !make_map(&prm.dmap, &prm.d_row0, &prm.d_rowts, a.Ds, a.Ds_ts, a.ntasks, a.M, a.lda, 4,
-                       TBM, false))
+                       BM, false))
     return cudaSuccess;
   if (!adj) {
     prm.d_row0 = prm.d_rowts = 0;
     prm.dmap = prm.amap;
   }
   *launched = true;
-  return adj ? launch_t<true>(prm, st) : launch_t<false>(prm, st);
+  if (kind == 1) return adj ? launch_t<TBigA>(prm, st) : launch_t<TBig>(prm, st);
+  return adj ? launch_t<TSmA>(prm, st) : launch_t<TSm>(prm, st);
 }
 
 }  // namespace lmg
