@@ -163,6 +163,28 @@ __global__ void k_halo_finish(const double* __restrict__ s0, const double* __res
     out[i] = __dadd_rn(s0 ? s0[i] : 0.0, adv[i]);
 }
 
+// device-side stopping test of the solve loop (multigrid.py:297-309 per sample): record this
+// cycle's norms for the samples still running; keep looping (the enclosing conditional WHILE graph
+// node) until some sample reaches tol or max_cycles -- the host then parks it and resumes
+__global__ void k_cycle_book(const double* __restrict__ norms, int B, double tol,
+                             const int* __restrict__ done, double* __restrict__ hist,
+                             int* __restrict__ cyc, int max_cycles, cudaGraphConditionalHandle h) {
+  __shared__ int any;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  const int c = *cyc + 1;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    if (done[b]) continue;
+    hist[(int64_t)c * B + b] = norms[b];
+    if (norms[b] <= tol) atomicOr(&any, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *cyc = c;
+    cudaGraphSetConditional(h, (!any && c < max_cycles) ? 1u : 0u);
+  }
+}
+
 // after a fused FCF sweep: U[0] = f[0] (c_relaxation, multigrid.py:157) and U[kc] = Cn[k], k >= 1
 __global__ void k_fcf_commit(double* __restrict__ U, const double* __restrict__ src0,
                              const double* __restrict__ Cn, int nb, int c, int64_t BQ) {
@@ -1480,8 +1502,105 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
       if (*g) cudaGraphExecDestroy(*g);
     }
   } guard{&gexec};
+  // Device-side loop (opt-in, LMG_DEVLOOP=1): cycles 2.. run inside a conditional WHILE graph
+  // node whose body is one cycle + k_cycle_book; the loop leaves the device only when some sample
+  // converges (to park it) or at max_cycles.  Correct (GPU tests pass with it), but measured
+  // SLOWER on this driver (580.159): c1 3.14 vs 2.15 ms, c5 26.5 vs 25.6 ms, c2 1.20 vs 1.08 s per
+  // step -- kernels in a conditional body pay ~17 us each -- so the per-cycle host test stays.
+  const bool dev_loop = use_graph && getenv("LMG_DEVLOOP") != nullptr;
+  cudaGraphExec_t dexec = nullptr;
+  struct GraphGuard2 {
+    cudaGraphExec_t* g;
+    ~GraphGuard2() {
+      if (*g) cudaGraphExecDestroy(*g);
+    }
+  } guard2{&dexec};
+  unsigned long long iter_launches = 0;
+  int* done_d = nullptr;
+  int* cyc_d = nullptr;
+  double* hist_d = nullptr;
+  struct DevFree {
+    int** a; int** b; double** c; cudaStream_t st;
+    ~DevFree() {
+      if (*a) cudaFreeAsync(*a, st);
+      if (*b) cudaFreeAsync(*b, st);
+      if (*c) cudaFreeAsync(*c, st);
+    }
+  } devfree{&done_d, &cyc_d, &hist_d, st};
+  std::vector<int> done_i(B);
+  std::vector<double> hrows;
   int cyc = 0;
   while (ndone < B && cyc < max_cycles) {
+    if (dev_loop && cyc > 0) {
+      if (!dexec) {
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&done_d), B * sizeof(int), st));
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&cyc_d), sizeof(int), st));
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&hist_d),
+                                 (size_t)(max_cycles + 1) * B * sizeof(double), st));
+        cudaGraph_t g;
+        CUDA_TRY(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle hnd;
+        CUDA_TRY(cudaGraphConditionalHandleCreate(&hnd, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = hnd;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        CUDA_TRY(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        const unsigned long long n0 = g_launches.load();
+        CUDA_TRY(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        int rc = cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, true);
+        if (rc == LMG_OK)
+          rc = launch(CLS_ELEM, 0.0, 0.0, st, [&] {
+            k_cycle_book<<<1, 256, 0, st>>>(ws.norms, B, tol, done_d, hist_d, cyc_d, max_cycles, hnd);
+          });
+        cudaGraph_t body_out = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(st, &body_out);
+        if (rc != LMG_OK) {
+          cudaGraphDestroy(g);
+          return rc;
+        }
+        if (ce != cudaSuccess) {
+          cudaGraphDestroy(g);
+          return fail(LMG_ERR_CUDA, std::string("loop capture: ") + cudaGetErrorString(ce));
+        }
+        iter_launches = g_launches.load() - n0;
+        g_launches -= iter_launches;  // counted per executed iteration below
+        ce = cudaGraphInstantiate(&dexec, g, 0);
+        cudaGraphDestroy(g);
+        if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("loop instantiate: ") + cudaGetErrorString(ce));
+      }
+      for (int b = 0; b < B; ++b) done_i[b] = done[b];
+      CUDA_TRY(cudaMemcpyAsync(done_d, done_i.data(), B * sizeof(int), cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaMemcpyAsync(cyc_d, &cyc, sizeof(int), cudaMemcpyHostToDevice, st));
+      CUDA_TRY(cudaGraphLaunch(dexec, st));
+      int newcyc = cyc;
+      CUDA_TRY(cudaMemcpyAsync(&newcyc, cyc_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      hrows.resize((size_t)(newcyc - cyc) * B);
+      CUDA_TRY(cudaMemcpyAsync(hrows.data(), hist_d + (int64_t)(cyc + 1) * B,
+                               hrows.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      g_launches += iter_launches * (unsigned long long)(newcyc - cyc);
+      int newly = 0;
+      for (int cc = cyc + 1; cc <= newcyc; ++cc)
+        for (int b = 0; b < B; ++b) {
+          if (done[b]) continue;
+          const double nv = hrows[(size_t)(cc - cyc - 1) * B + b];
+          hist_host[(int64_t)cc * B + b] = nv;
+          cycles_host[b] = cc;
+          if (cc == newcyc && nv <= tol) { done[b] = 1; ++newly; }
+        }
+      cyc = newcyc;
+      ndone += newly;
+      if (newly && ndone < B)
+        for (int b = 0; b < B; ++b)
+          if (done[b] && std::none_of(parked.begin(), parked.end(), [&](auto& pb) { return pb.first == b; }))
+            TRY(park(b));
+      continue;
+    }
     if (use_graph && cyc > 0) {
       if (!gexec) {
         cudaGraph_t graph;
