@@ -391,6 +391,21 @@ def run_ours(args, cfg):
         barrier()
         serial_ms = s3.elapsed_time(e3) / args.steps
         del Us
+    elif not conv:
+        # model-partitioned serial propagation over the same ranks: each rank
+        # propagates its layers and hands the state on; timed like the FAS step (max over ranks)
+        tr.serial_step(X, labels)
+        barrier()
+        s3, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s3.record()
+        for _ in range(args.steps):
+            tr.serial_step(X, labels)
+        e3.record()
+        barrier()
+        serial_ms = s3.elapsed_time(e3) / args.steps
+        t = torch.tensor([serial_ms], device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        serial_ms = float(t.item())
 
     # ---- e2e: same step through the public API from pinned host buffers, result read back
     barrier()
@@ -452,9 +467,12 @@ def run_ours(args, cfg):
     if serial_ms is not None:
         line["serial_gpu"] = dict(
             value=N * B / (serial_ms * 1e-3), unit=UNIT, ms_per_step=serial_ms,
-            what="layer-by-layer GPU propagation of the same step with the same kernels: "
-                 "sequential_forward (network.py:111-123) + the reference's sequential adjoint "
-                 "(training.py:216-224) + gradients + SGD",
+            what=("layer-by-layer GPU propagation of the same step with the same kernels: "
+                  "sequential_forward (network.py:111-123) + the reference's sequential adjoint "
+                  "(training.py:216-224) + gradients + SGD"
+                  + ("" if world == 1 else
+                     f"; model-partitioned over {world} ranks (each rank propagates its layers "
+                     "and hands the state to the next, LayerParallelTrainer.serial_step)")),
             fas_over_serial_time=ms / serial_ms)
     line["clocks"] = clk.summary()
     if rank == 0:

@@ -440,3 +440,63 @@ class LayerParallelTrainer:
         if loss is None:
             loss = t.zeros(B, dtype=t.float64, device=self.device)
         return StepResult(loss, hist, cyc, conv, ahist, acyc, aconv)
+
+    def serial_step(self, X, labels):
+        """Model-partitioned serial baseline (the north_star comparison): no
+        multigrid -- layer-by-layer propagation with the layer axis split over the ranks.  Rank r
+        waits for rank r-1's propagated last state, runs sequential_forward over its L layers
+        (network.py:111-123) and hands the next state on (one (B, q) message per edge); the
+        reference's sequential adjoint (training.py:216-224) runs back the same way, then the
+        block gradients + SGD.  Same kernels and buffers as step()."""
+        from .training import _dense_apply, _dense_vjp, softmax_ce
+
+        t = self.t
+        B = X.shape[0]
+        self._setup(B)
+        st = _lib.stream_handle()
+        view = self._view
+        first, last = self.rank == 0, self.rank == self.world - 1
+        fw, aw = self._fwd, self._adj
+        L, q = self.L, self.q
+        if first:
+            head = _dense_apply(self.dnet.Wo, self.dnet.bo, self.dnet.open_act, X)
+        else:
+            fw._exchange(None, fw.recv1)
+            head = fw.recv1[0]
+        _lib.call("lmg_sequential_forward", view.desc(), B, head.data_ptr(), _lib.SRC_HEAD,
+                  self.U.data_ptr(), st)
+        nxt = t.empty((1, B, q), dtype=t.float64, device=self.device)
+        _lib.call("lmg_propagate", view.desc(), B, self.U[L - 1].data_ptr(), None, _lib.SRC_HEAD,
+                  L, L + 1, nxt.data_ptr(), st)
+        if not last:
+            fw._exchange(nxt, None)
+        _lib.call("lmg_act_deriv", view.desc(), B, self.U.data_ptr(), self.D.data_ptr(), st)
+        loss = None
+        if last:  # output_state -> logits -> softmax CE (training.py:210-213)
+            logits = _dense_apply(self.dnet.Wr, self.dnet.br, self.dnet.read_act, nxt[0])
+            loss, dl = softmax_ce(logits, labels)
+            ahead, gWr, gbr = _dense_vjp(self.dnet.Wr, self.dnet.br, self.dnet.read_act, nxt[0], dl)
+        else:
+            aw._exchange(None, aw.recv1)
+            ahead = aw.recv1[0]
+        _lib.call("lmg_sequential_forward", view.desc(self.D), B, ahead.data_ptr(), _lib.SRC_HEAD,
+                  self.lam.data_ptr(), st)
+        out = t.empty((1, B, q), dtype=t.float64, device=self.device)
+        _lib.call("lmg_propagate", view.desc(self.D), B, self.lam[L - 1].data_ptr(), None,
+                  _lib.SRC_HEAD, L, L + 1, out.data_ptr(), st)
+        scale = 1.0 / B
+        if not first:
+            aw._exchange(out, None)
+        else:  # lambda^0 -> opening gradient
+            _, gWo, gbo = _dense_vjp(self.dnet.Wo, self.dnet.bo, self.dnet.open_act, X, out[0],
+                                     want_gx=False)
+        _lib.call("lmg_param_grads", view.desc(), B, self.U.data_ptr(), self.lam.data_ptr(),
+                  self.D.data_ptr(), scale, float(self.lr), None, None, st)
+        if first and self.lr:
+            self.dnet.Wo.sub_(gWo * (scale * self.lr))
+            self.dnet.bo.sub_(gbo * (scale * self.lr))
+        if last and self.lr:
+            self.dnet.Wr.sub_(gWr * (scale * self.lr))
+            self.dnet.br.sub_(gbr * (scale * self.lr))
+        return loss if loss is not None else t.zeros(B, dtype=t.float64, device=self.device)
+

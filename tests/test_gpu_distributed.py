@@ -129,3 +129,62 @@ def test_partitioned_training_step_bitwise_vs_single_gpu(tmp_path):
         assert np.array_equal(r["ahist"], ref["ahist"][: ref["acyc"].max() + 1], equal_nan=True), world
         assert r["W"].tobytes() == ref["W"].tobytes(), world
         assert np.array_equal(r["loss"], ref["loss"]), world
+
+
+def _serial_worker(rank, world, port, out):
+    sys.path.insert(0, ROOT)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    from paper_2007_07336_b200.distributed import LayerParallelTrainer
+
+    X, labels = _inputs()
+    tr = LayerParallelTrainer(N, Q, [3, N, Q], coarsening=C, threshold=THR, learning_rate=0.1)
+    loss = tr.serial_step(torch.from_numpy(X).cuda(), torch.from_numpy(labels).cuda()).cpu()
+    W = tr.dnet.stack.W.cpu()
+    wparts = [torch.empty_like(W) for _ in range(world)]
+    dist.all_gather(wparts, W)
+    dist.broadcast(loss, src=world - 1)
+    if rank == 0:
+        with open(out, "wb") as fh:
+            pickle.dump(dict(W=torch.cat(wparts).numpy(), loss=loss.numpy()), fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _serial_single(rank, out):
+    sys.path.insert(0, ROOT)
+    torch.cuda.set_device(0)
+    import paper_2007_07336_b200 as P
+    from paper_2007_07336_b200 import _lib
+    from paper_2007_07336_b200.training import _dense_apply, backward
+
+    X, labels = _inputs()
+    d = P.device_network(N, Q, [3, N, Q])
+    Xt, lt = torch.from_numpy(X).cuda(), torch.from_numpy(labels).cuda()
+    U = torch.empty((N, X.shape[0], Q), dtype=torch.float64, device="cuda")
+    f0 = _dense_apply(d.Wo, d.bo, d.open_act, Xt)
+    _lib.call("lmg_sequential_forward", d._lmg_view().desc(), X.shape[0], f0.data_ptr(), _lib.SRC_HEAD,
+              U.data_ptr(), _lib.stream_handle())
+    r = backward(d, U, Xt, lt, adjoint="sequential", scale=1.0 / X.shape[0], lr=0.1, want_grads=False)
+    with open(out, "wb") as fh:
+        pickle.dump(dict(W=d.stack.W.cpu().numpy(), loss=r.loss.cpu().numpy()), fh)
+
+
+def test_partitioned_serial_baseline_matches_single_gpu(tmp_path):
+    """LayerParallelTrainer.serial_step (the model-partitioned serial baseline of bench.py at
+    N > 1) is bitwise the single-GPU sequential forward + sequential adjoint + SGD step with the
+    launch-per-step kernels."""
+    old = os.environ.get("LMG_NO_SPLITK")
+    os.environ["LMG_NO_SPLITK"] = "1"  # one k-ascending chain everywhere (spawned processes)
+    try:
+        ref = _spawn(_serial_single, (str(tmp_path / "s1.pkl"),), 1, str(tmp_path / "s1.pkl"))
+        for world in (2, 4):
+            out = str(tmp_path / f"sw{world}.pkl")
+            r = _spawn(_serial_worker, (world, _port(), out), world, out)
+            assert r["W"].tobytes() == ref["W"].tobytes(), world
+            assert np.array_equal(r["loss"], ref["loss"]), world
+    finally:
+        if old is None:
+            del os.environ["LMG_NO_SPLITK"]
+        else:
+            os.environ["LMG_NO_SPLITK"] = old
