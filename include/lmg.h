@@ -83,6 +83,9 @@ int lmg_timing_read(int cls, double* ms_total, double* flops_total, double* byte
  * stamps (step start, state ready, mainloop done, epilogue done) of chain 0 / CTA 0 of every
  * fused persistent sweep launch.  Classes 4/5 of lmg_timing_read are those launches. */
 int lmg_debug_sweep_trace(unsigned long long* dev_buf);
+/* Debug: co-resident clusters of a fused-sweep configuration (cfg 0: 64 columns per CTA,
+ * 1: 32) at width q, from cudaOccupancyMaxActiveClusters; negative on error. */
+int lmg_debug_sweep_clusters(int q, int adj, int cfg);
 
 /* network.py:88-102 propagate_values: out[j-start] = src[j] + (u + h*F_{j-1}(u)), j in
  * [start, stop), from u_start (B, q) = u^{start-1}.  out is (stop-start, B, q). */

@@ -57,6 +57,7 @@ SIGNATURES = {
     "lmg_launch_count": (ctypes.c_ulonglong, []),
     "lmg_timing_enable": (_I, [_I]),
     "lmg_debug_sweep_trace": (_I, [_P]),
+    "lmg_debug_sweep_clusters": (_I, [_I, _I, _I]),
     "lmg_timing_read": (_I, [_I, c_double_p, c_double_p, c_double_p,
                              ctypes.POINTER(ctypes.c_ulonglong)]),
     "lmg_propagate": (_I, [_SYS, _I, _P, _P, _I, _I, _I, _P, _P]),

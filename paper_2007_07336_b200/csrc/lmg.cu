@@ -751,6 +751,19 @@ SweepArgs sweep_args(const lmg_system& S, int B, int mode, int c, const double* 
   return a;
 }
 
+// co-resident clusters of a sweep configuration, cached per (q, adjoint, cfg)
+int sweep_clusters(int q, int adj, int cfg) {
+  static std::mutex mu;
+  static std::vector<std::pair<int64_t, int>> cache;
+  const int64_t key = ((int64_t)q << 8) | (adj << 4) | cfg;
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& kv : cache)
+    if (kv.first == key) return kv.second;
+  const int n = sweep_max_clusters(q, adj, cfg);
+  cache.emplace_back(key, n);
+  return n;
+}
+
 // algorithmic work of one sweep launch: `steps` layer steps over the whole batch, `written`
 // state rows stored to HBM (2q^2+5q flops per F-evaluation; W read once per step)
 int run_sweep(const SweepArgs& a, const SweepShape& sh, double steps, double written, cudaStream_t st) {
@@ -772,9 +785,12 @@ int seq_sweep(const lmg_system& S, int B, const double* src, int mode, double* U
   SweepArgs a = sweep_args(S, B, SW_SEQ, 1, src, mode, U);
   SweepShape sh;
   if (sweep_shape(a, &sh) < 0) return -1;
-  // one wave of 16-CTA clusters only: beyond that (B > 144) the split-K per-step path measured
-  // faster (B = 256, 64 steps: 12.4 vs 18.7 us per step with 8-CTA clusters in two waves)
-  if ((int64_t)sh.grid.y * sh.cs > 148) return -1;
+  // one wave of clusters only (cudaOccupancyMaxActiveClusters: at q = 512 on B200, 7 clusters of
+  // 16 CTAs or 15 of 8): beyond that the split-K per-step path measured faster (B = 256, 64
+  // steps: 12.4 vs 18.7 us per step with 8-CTA clusters in two waves)
+  if ((int)sh.grid.y > sweep_clusters(S.width, a.adj, sh.cfg) && sh.cfg == 1)
+    if (sweep_shape(a, &sh, 0) < 0) return -1;
+  if ((int)sh.grid.y > sweep_clusters(S.width, a.adj, sh.cfg)) return -1;
   const int64_t BQ = (int64_t)B * S.width;
   TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]
   return run_sweep(a, sh, S.num_layers - 1, S.num_layers - 1, st);
@@ -799,7 +815,7 @@ int fcf_sweep(const lmg_system& S, int B, int c, double* U, const double* src, i
   // clusters).  With more chains than that the per-step launches keep all SMs streaming W and
   // measured faster (c5 fine level: 64 chains x 8 CTAs).  LMG_SWEEP_ALL=1 lifts the limit.
   static const bool all = getenv("LMG_SWEEP_ALL") != nullptr;
-  if (!all && (int64_t)sh.grid.x * sh.grid.y * sh.grid.z > 148) return -1;
+  if (!all && (int)(sh.grid.y * sh.grid.z) > sweep_clusters(S.width, a.adj, sh.cfg)) return -1;
   double steps = (c - 1) + (nb > 1 ? 1 : 0), written = steps;
   for (int k = 1; k < nb; ++k) {
     const int r0 = (k - 1) * c + (Q ? 1 : 0);
@@ -1294,6 +1310,8 @@ const char* lmg_last_error(void) { return g_err.c_str(); }
 
 // debug instrumentation: device buffer (>= 4 * steps u64) receiving per-step globaltimer stamps
 // (step start, state ready, mainloop done, epilogue done) of chain 0 / CTA 0 of every fused sweep
+int lmg_debug_sweep_clusters(int q, int adj, int cfg) { return sweep_max_clusters(q, adj, cfg); }
+
 int lmg_debug_sweep_trace(unsigned long long* dev_buf) {
   g_sweep_trace = dev_buf;
   return LMG_OK;

@@ -504,4 +504,38 @@ cudaError_t sweep_launch(const SweepArgs& a, const SweepShape& s, cudaStream_t s
   return a.adj ? launch_c<Cfg32A>(a, s, st) : launch_c<Cfg32F>(a, s, st);
 }
 
+// how many clusters of a configuration can be co-resident (cudaOccupancyMaxActiveClusters)
+int sweep_max_clusters(int q, int adj, int cfg) {
+  SweepArgs a{};
+  a.mode = SW_SEQ; a.B = 16; a.q = q; a.n = 2; a.adj = adj;
+  SweepShape sh;
+  if (sweep_shape(a, &sh, cfg) < 0) return -1;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(sh.cs, 64, 1);
+  lc.blockDim = dim3(sh.nthreads, 1, 1);
+  lc.dynamicSmemBytes = sh.smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = sh.cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  int n = -1;
+  cudaError_t e;
+  if (sh.cfg == 0) {
+    auto k = adj ? sweep_kernel<Cfg64A> : sweep_kernel<Cfg64F>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaOccupancyMaxActiveClusters(&n, k, &lc);
+  } else {
+    auto k = adj ? sweep_kernel<Cfg32A> : sweep_kernel<Cfg32F>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+    cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaOccupancyMaxActiveClusters(&n, k, &lc);
+  }
+  return e == cudaSuccess ? n : -(int)e;
+}
+
 }  // namespace lmg
+

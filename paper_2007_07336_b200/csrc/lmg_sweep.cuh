@@ -54,5 +54,6 @@ struct SweepShape {
 // forced_cfg >= 0 picks a configuration (0: 64 columns per CTA, 1: 32) instead of the default
 int sweep_shape(const SweepArgs& a, SweepShape* s, int forced_cfg = -1);
 cudaError_t sweep_launch(const SweepArgs& a, const SweepShape& s, cudaStream_t st);
+int sweep_max_clusters(int q, int adj, int cfg);
 
 }  // namespace lmg
