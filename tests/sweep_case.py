@@ -1,7 +1,7 @@
 """Run one FAS training step on cuda:0 and save everything it produced (helper of
 tests/test_gpu_sweep.py; run in a subprocess so LMG_* routing variables take effect).
 
-    python tests/sweep_case.py N q B c threshold out.npz
+    python tests/sweep_case.py N q B c threshold out.npz [activation]
 """
 import os
 import sys
@@ -14,11 +14,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def main():
     N, q, B, c, thr = (int(v) for v in sys.argv[1:6])
     out = sys.argv[6]
+    act = sys.argv[7] if len(sys.argv) > 7 else "tanh"
     import torch
 
     import paper_2007_07336_b200 as P
 
-    d = P.device_network(N, q, [0, N, q], device="cuda:0")
+    d = P.device_network(N, q, [0, N, q], device="cuda:0", activation=act)
     X = torch.from_numpy(P.random_batch(q, [0, N, q], B)).cuda()
     labels = torch.from_numpy(np.arange(B) % 10).cuda()
     tr = P.DeviceTrainer(d, coarsening=c, threshold=thr if thr > 0 else None, tol=1e-9,

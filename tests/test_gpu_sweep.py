@@ -28,6 +28,8 @@ CASES = [
     (128, 256, 20, 4, 8),    # two batch tiles (20 = 16 + 4 masked rows), 3 levels
     (96, 64, 33, 2, 12),     # cf 2, three batch tiles, 4 levels [96,48,24,12]
     (64, 512, 160, 4, 16),   # B > 64: per-step FCF, serial coarsest solve on 10 batch tiles
+    (128, 128, 12, 4, 8, "relu"),      # the other fused activations
+    (64, 256, 16, 4, 0, "identity"),
 ]
 
 
@@ -35,7 +37,8 @@ def _run(case, tmp_path, env_extra):
     tag = "_".join("%s%s" % kv for kv in sorted(env_extra.items())) or "default"
     out = str(tmp_path / ("%s_%s.npz" % ("_".join(map(str, case)), tag)))
     env = dict(os.environ, **env_extra)
-    subprocess.run([sys.executable, os.path.join(HERE, "sweep_case.py"), *map(str, case), out],
+    subprocess.run([sys.executable, os.path.join(HERE, "sweep_case.py"), *map(str, case[:5]), out,
+                    *(case[5:] or ["tanh"])],
                    check=True, env=env, timeout=600)
     return np.load(out)
 
@@ -45,7 +48,7 @@ def _close(a, b, rel):
     return float(np.nanmax(np.abs(a - b))) <= rel * scale
 
 
-@pytest.mark.parametrize("case", CASES, ids=lambda c: "N%d_q%d_B%d_c%d" % c[:4])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "N%d_q%d_B%d_c%d" % c[:4] + "".join("_" + x for x in c[5:]))
 def test_fused_sweep_matches_per_step(case, tmp_path):
     off = _run(case, tmp_path, {"LMG_NO_SWEEP": "1"})
     on = _run(case, tmp_path, {})
