@@ -180,6 +180,16 @@ int lmg_local_fcf_a(const lmg_system* sys, int B, int c, double* U, const double
 int lmg_local_fcf_b(const lmg_system* sys, int B, int c, double* U, const double* src,
                     int src_mode, double* P, int has_next, double* adv_out, double* advH,
                     void* stream);
+/* Layer-partitioned FCF (the rank's run of blocks) as fused persistent sweeps: part 0 runs every
+ * chain that needs no halo -- with has_next its halo chain writes the next rank's incoming C row
+ * (no source) to states[L] -- and commits the new C rows; part 1, after the exchange and
+ * lmg_halo_finish of states[0], runs block 0 of a non-first rank and copies advH[nb-1] to adv_out.
+ * Same outputs as lmg_local_fcf_a/_b (parallel.py:143-241).  Cn: nb*(B,q) scratch.
+ * lmg_local_fcf_fused_ok returns 1 when this path applies (small batch, one wave of clusters). */
+int lmg_local_fcf_fused_ok(const lmg_system* sys, int B, int c, int is_first, int has_next);
+int lmg_local_fcf_fused(const lmg_system* sys, int B, int c, double* states, const double* src,
+                        int src_mode, int is_first, int has_next, const double* Q, double* P,
+                        double* advH, double* Cn, int part, double* adv_out, void* stream);
 int lmg_halo_finish(const double* s0, const double* adv_in, double* out, int64_t len, void* stream);
 int lmg_local_coarse_source(const lmg_system* sys, int B, int c, const double* U,
                             const double* src, int src_mode, const double* P,

@@ -80,6 +80,8 @@ SIGNATURES = {
     "lmg_param_grads_ex": (_I, [_SYS, _I, _P, _P, _P, _D, _D, _P, _P, _I, _P]),
     "lmg_local_fcf_a": (_I, [_SYS, _I, _I, _P, _P, _I, _I, _I, _P, _P]),
     "lmg_local_fcf_b": (_I, [_SYS, _I, _I, _P, _P, _I, _P, _I, _P, _P, _P]),
+    "lmg_local_fcf_fused_ok": (_I, [_SYS, _I, _I, _I, _I]),
+    "lmg_local_fcf_fused": (_I, [_SYS, _I, _I, _P, _P, _I, _I, _I, _P, _P, _P, _P, _I, _P, _P]),
     "lmg_halo_finish": (_I, [_P, _P, _P, ctypes.c_int64, _P]),
     "lmg_local_coarse_source": (_I, [_SYS, _I, _I, _P, _P, _I, _P, _P, _I, _P, _P, _P, _P]),
     "lmg_local_correct": (_I, [_I, _I, _I, _I, _P, _P, _P]),

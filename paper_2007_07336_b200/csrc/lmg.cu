@@ -192,6 +192,7 @@ __global__ void k_fcf_commit(double* __restrict__ U, const double* __restrict__ 
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / BQ, i = e - r * BQ;
+    if (r == 0 && !src0) continue;  // row 0 already finished from the incoming halo
     U[r * c * BQ + i] = r == 0 ? src0[i] : Cn[e];
   }
 }
@@ -748,6 +749,7 @@ SweepArgs sweep_args(const lmg_system& S, int B, int mode, int c, const double* 
   a.src = src; a.src_head = src_mode == LMG_SRC_HEAD;
   a.U = U;
   a.trace = g_sweep_trace;
+  a.is_first = 1;
   return a;
 }
 
@@ -829,6 +831,84 @@ int fcf_sweep(const lmg_system& S, int B, int c, double* U, const double* src, i
   return launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
     k_fcf_commit<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, src, Cn, nb, c, BQ);
   });
+}
+
+// Layer-partitioned FCF as fused sweeps (one rank's run of blocks).  part 0: every chain that
+// needs no halo -- blocks 1..nb-1, block 0 on the first rank, and with has_next the halo chain
+// whose last row (the next rank's C row, no source) lands in U[L] -- then the C-row commit;
+// part 1 (after the halo exchange and lmg_halo_finish of U[0]): block 0 of a non-first rank, and
+// adv_out = advH[nb-1] for the next rank's coarse source.  Same layer steps on the same operands
+// as local_fcf_a + local_fcf_b.
+SweepArgs local_fused_args(const lmg_system& S, int B, int c, double* U, const double* src, int mode,
+                           bool is_first, bool has_next, const double* Q, double* P, double* advH,
+                           double* Cn, int part) {
+  const int nb = S.num_layers / c;
+  SweepArgs a = sweep_args(S, B, SW_FCF, c, src, mode, U);
+  a.h2 = S.step * c;
+  a.Q = Q; a.Cn = Cn; a.P = P; a.advH = advH;
+  a.is_first = is_first ? 1 : 0;
+  a.has_next = has_next ? 1 : 0;
+  a.halo = U + (int64_t)S.num_layers * B * S.width;
+  if (part == 0) {
+    a.k0 = is_first ? 0 : 1;
+    a.nchains = nb + (has_next ? 1 : 0) - a.k0;
+  } else {
+    a.k0 = 0;
+    a.nchains = is_first ? 0 : 1;
+  }
+  return a;
+}
+
+bool local_fused_ok(const lmg_system& S, int B, int c, bool is_first, bool has_next) {
+  if (B > sweep_max_batch() || !sweep_basic_ok(S) || S.num_layers % c) return false;
+  const int nb = S.num_layers / c;
+  SweepArgs a = local_fused_args(S, B, c, nullptr, nullptr, LMG_SRC_HEAD, is_first, has_next,
+                                 nullptr, nullptr, nullptr, nullptr, 0);
+  if (a.nchains <= 0) a.nchains = 1;
+  SweepShape sh;
+  if (sweep_shape(a, &sh) < 0) return false;
+  static const bool all = getenv("LMG_SWEEP_ALL") != nullptr;
+  if (!all && (int)(sh.grid.y * sh.grid.z) > sweep_clusters(S.width, a.adj, sh.cfg)) return false;
+  (void)nb;
+  return true;
+}
+
+int local_fcf_fused(const lmg_system& S, int B, int c, double* U, const double* src, int mode,
+                    bool is_first, bool has_next, const double* Q, double* P, double* advH,
+                    double* Cn, int part, double* adv_out, cudaStream_t st) {
+  const int nb = S.num_layers / c;
+  const int64_t BQ = (int64_t)B * S.width;
+  if (!aligned16(src) || !aligned16(U) || !aligned16(Q) || !aligned16(P) || !aligned16(advH) ||
+      !aligned16(Cn) || !P || !Cn || (is_first && !src))
+    return fail(LMG_ERR_CONFIGURATION, "fused FCF: missing or misaligned buffers");
+  SweepArgs a = local_fused_args(S, B, c, U, src, mode, is_first, has_next, Q, P, advH, Cn, part);
+  if (a.nchains > 0) {
+    SweepShape sh;
+    if (sweep_shape(a, &sh) < 0) return fail(LMG_ERR_CONFIGURATION, "fused FCF not available");
+    double steps = 0.0, written = 0.0;
+    for (int k = a.k0; k < a.k0 + a.nchains; ++k) {
+      const bool p_step = k < nb - 1 || has_next;
+      if (k == 0) {
+        steps += (c - 1) + (p_step ? 1 : 0);
+        written += (c - 1) + (p_step ? 1 : 0);
+        continue;
+      }
+      const int r0 = (k - 1) * c + (Q ? 1 : 0);
+      const int last = k == nb ? nb * c : k * c + c - 1 + (p_step ? 1 : 0);
+      steps += last - r0;
+      written += k == nb ? 1 : c + (p_step ? 1 : 0);
+    }
+    if (advH) written += a.nchains;
+    TRY(run_sweep(a, sh, steps, written, st));
+  }
+  if (part == 0 && nb > 0) {  // U[0] = f[0] on the first rank; U[kc] = Cn[k], k = 1..nb-1
+    TRY(launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
+      k_fcf_commit<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, is_first ? src : nullptr, Cn, nb, c, BQ);
+    }));
+  }
+  if (part == 1 && has_next && adv_out && advH)
+    TRY(copy_rows(adv_out, 0, advH + (int64_t)(nb - 1) * BQ, 0, 1, BQ, st));
+  return LMG_OK;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1791,6 +1871,21 @@ int lmg_local_fcf_b(const lmg_system* sys, int B, int c, double* U, const double
   TRY(check_sys(sys, B));
   TRY(check_levels(*sys, 2, c));
   return local_fcf_b(*sys, B, c, U, src, src_mode, P, has_next != 0, adv_out, S_(stream), advH);
+}
+
+int lmg_local_fcf_fused_ok(const lmg_system* sys, int B, int c, int is_first, int has_next) {
+  if (check_sys(sys, B) != LMG_OK || check_levels(*sys, 2, c) != LMG_OK) return 0;
+  return local_fused_ok(*sys, B, c, is_first != 0, has_next != 0) ? 1 : 0;
+}
+
+int lmg_local_fcf_fused(const lmg_system* sys, int B, int c, double* U, const double* src,
+                        int src_mode, int is_first, int has_next, const double* Q, double* P,
+                        double* advH, double* Cn, int part, double* adv_out, void* stream) {
+  TRY(check_sys(sys, B));
+  TRY(check_levels(*sys, 2, c));
+  if (part != 0 && part != 1) return fail(LMG_ERR_CONFIGURATION, "part must be 0 or 1");
+  return local_fcf_fused(*sys, B, c, U, src, src_mode, is_first != 0, has_next != 0, Q, P, advH, Cn,
+                         part, adv_out, S_(stream));
 }
 
 int lmg_halo_finish(const double* s0, const double* adv_in, double* out, int64_t len, void* stream) {

@@ -91,10 +91,11 @@ __device__ __forceinline__ Chain chain_of(const SweepArgs& a, int k, int64_t BQ)
     return ch;
   }
   const int c = a.c, nb = a.n / c;
+  const bool p_last = a.has_next || nb > 1;  // block nb-1 / chain k < nb-1 has a P step
   if (k == 0) {
     ch.r0 = 0;
-    ch.start = a.src;  // f[0]
-    ch.nsteps = (c - 1) + (nb > 1 ? 1 : 0);
+    ch.start = a.is_first ? a.src : a.U;  // f[0], or U[0] finished from the incoming halo
+    ch.nsteps = (c - 1) + (p_last ? 1 : 0);
     return ch;
   }
   if (a.Q) {
@@ -104,7 +105,9 @@ __device__ __forceinline__ Chain chain_of(const SweepArgs& a, int k, int64_t BQ)
     ch.r0 = (k - 1) * c;
     ch.start = a.U + (int64_t)ch.r0 * BQ;
   }
-  ch.nsteps = (k * c + c - 1 + (k < nb - 1 ? 1 : 0)) - ch.r0;
+  const int lastrow = k == nb ? nb * c  // halo chain: up to the next rank's C row
+                              : k * c + c - 1 + ((k < nb - 1 || a.has_next) ? 1 : 0);
+  ch.nsteps = lastrow - ch.r0;
   return ch;
 }
 
@@ -113,7 +116,7 @@ __device__ __forceinline__ double* dest_of(const SweepArgs& a, int k, int j, int
   if (a.mode == SW_SEQ) return a.U + (int64_t)j * BQ;
   const int c = a.c;
   if (j < k * c) return nullptr;
-  if (j == k * c) return a.Cn + (int64_t)k * BQ;  // k >= 1 here (k = 0 starts at row 0)
+  if (j == k * c) return k == a.n / c ? a.halo : a.Cn + (int64_t)k * BQ;  // k >= 1 here
   if (j < (k + 1) * c) return a.U + (int64_t)j * BQ;
   return a.P + (int64_t)(k + 1) * BQ;
 }
@@ -155,7 +158,7 @@ __global__ void __launch_bounds__(C::NT, 1) sweep_kernel(const __grid_constant__
   uint64_t* sready = empty + ST;                 // [2]: peer slices of A[buf] have landed
 
   const int n0 = rank * NC;
-  const int k = blockIdx.z;
+  const int k = a.k0 + (int)blockIdx.z;
   const int m0 = blockIdx.y * SW_BM;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t BQ = (int64_t)a.B * q;
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(C::NT, 1) sweep_kernel(const __grid_constant__
         }
       }
     }
-    const bool tr = a.trace && tid == 0 && k == 0 && rank == 0 && blockIdx.y == 0;
+    const bool tr = a.trace && tid == 0 && blockIdx.z == 0 && rank == 0 && blockIdx.y == 0;
     if (tr) a.trace[4 * s] = gtimer();
     if (s > 0) mbar_wait(&sready[cur], (uint32_t)((s - 1) >> 1) & 1u);
     if (tr) a.trace[4 * s + 1] = gtimer();
@@ -483,7 +486,7 @@ int sweep_config(int q, int B, int adj, int nchains) {
 }
 
 int sweep_shape(const SweepArgs& a, SweepShape* s, int forced_cfg) {
-  const int nchains = a.mode == SW_SEQ ? 1 : a.n / a.c;
+  const int nchains = a.mode == SW_SEQ ? 1 : (a.nchains > 0 ? a.nchains : a.n / a.c);
   const int mt = (a.B + SW_BM - 1) / SW_BM;
   int cfg = sweep_config(a.q, a.B, a.adj, nchains);
   if (forced_cfg == 0 && (a.adj ? fits<Cfg64A>(a.q) : fits<Cfg64F>(a.q))) cfg = 0;

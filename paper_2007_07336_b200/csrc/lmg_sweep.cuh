@@ -41,6 +41,13 @@ struct SweepArgs {
   double* P;                          // SW_FCF: P[k+1] = propagate(U[(k+1)c-1]) (P + (k+1)*BQ)
   double* advH;                       // SW_FCF: advH[k] = U[kc] + h2*F(U[kc]), nullable
   unsigned long long* trace;          // debug: per-step globaltimer stamps of chain 0, rank 0
+  // layer-partitioned FCF (a rank's run of blocks): chains k0 .. k0+gridDim.z-1; chain 0 starts
+  // at U[0] (already finished from the previous rank's halo) unless is_first; with has_next,
+  // chain nb is the halo chain -- block nb-1's first F rows, then row nb*c (the next rank's
+  // incoming C row, source row nb*c = the zero row) -> halo -- and block nb-1 gets its P step
+  int k0, is_first, has_next;
+  double* halo;
+  int nchains;  // chains in this launch (0: all nb of the level)
 };
 
 // configuration the launcher would use for (q, B, adj), or -1 if the fused sweep cannot run it

@@ -57,6 +57,20 @@ class CudaOps:
         _lib.call("lmg_local_fcf_b", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
                   P.data_ptr(), int(has_next), self._p(adv_out), self._p(advH), self._st())
 
+    def fused_ok(self, lv, is_first, has_next):
+        """1 if the level's FCF runs as fused persistent sweeps (lmg_local_fcf_fused)."""
+        key = (id(lv), bool(is_first), bool(has_next))
+        cache = self.__dict__.setdefault("_fused_cache", {})
+        if key not in cache:
+            cache[key] = bool(_lib.load().lmg_local_fcf_fused_ok(lv.desc(), lv.B, lv.c, int(is_first),
+                                                                 int(has_next)))
+        return cache[key]
+
+    def fcf_fused(self, lv, U, S, smode, is_first, has_next, Q, P, advH, Cn, part, adv_out):
+        _lib.call("lmg_local_fcf_fused", lv.desc(), lv.B, lv.c, U.data_ptr(), self._p(S), smode,
+                  int(is_first), int(has_next), self._p(Q), P.data_ptr(), self._p(advH),
+                  Cn.data_ptr(), int(part), self._p(adv_out), self._st())
+
     def halo_finish(self, s0, adv, out):
         _lib.call("lmg_halo_finish", self._p(s0), adv.data_ptr(), out.data_ptr(), out.numel(),
                   self._st())
@@ -184,6 +198,14 @@ class DistSolver:
         self.nblocks_total = nbt
         self.messages = 0  # halo messages sent by this rank (protocol accounting)
 
+    def _cn(self, l, lev):
+        """Scratch for the fused sweep's new C rows at level l (allocated on first use)."""
+        cn = self.__dict__.setdefault("_cn_bufs", {})
+        if l not in cn:
+            cn[l] = self.t.empty(max(lev.nb, 1), self.B, lev.q, dtype=self.t.float64,
+                                 device=self.device)
+        return cn[l]
+
     # -- point-to-point halo: send `send` to next, receive into `recv` from prev -------------------
     def _host_staged(self):
         """gloo moves only host tensors: stage device halos through host memory (used to run
@@ -255,13 +277,26 @@ class DistSolver:
         ops = self.ops
         nb, c = lev.nb, self.c
         P = self.P[l]
-        ops.fcf_a(lev, U, S, smode, self.is_first, self.has_next,
-                  self.Q if (l == 0 and self.q_valid) else None)
-        self._exchange(U[lev.L : lev.L + 1] if self.has_next else None, self.recv1)
-        if not self.is_first:
-            ops.halo_finish(None if S is None else S[0], self.recv1[0], U[0])
+        Qs = self.Q if (l == 0 and self.q_valid) else None
         adv_out = P[nb + 1] if self.has_next else None
-        ops.fcf_b(lev, U, S, smode, P, self.has_next, adv_out, self.advH[l])
+        fused = getattr(ops, "fused_ok", None)
+        if fused is not None and fused(lev, self.is_first, self.has_next):
+            # fused persistent sweeps: every chain that needs no halo (incl. the halo chain that
+            # produces U[L]), the exchange, then block 0 from the finished U[0]
+            Cn = self._cn(l, lev)
+            ops.fcf_fused(lev, U, S, smode, self.is_first, self.has_next, Qs, P, self.advH[l], Cn, 0,
+                          None)
+            self._exchange(U[lev.L : lev.L + 1] if self.has_next else None, self.recv1)
+            if not self.is_first:
+                ops.halo_finish(None if S is None else S[0], self.recv1[0], U[0])
+            ops.fcf_fused(lev, U, S, smode, self.is_first, self.has_next, Qs, P, self.advH[l], Cn, 1,
+                          adv_out)
+        else:
+            ops.fcf_a(lev, U, S, smode, self.is_first, self.has_next, Qs)
+            self._exchange(U[lev.L : lev.L + 1] if self.has_next else None, self.recv1)
+            if not self.is_first:
+                ops.halo_finish(None if S is None else S[0], self.recv1[0], U[0])
+            ops.fcf_b(lev, U, S, smode, P, self.has_next, adv_out, self.advH[l])
         self._exchange(P[nb : nb + 2] if self.has_next else None, self.recv2)
         if not self.is_first:
             ops.halo_finish(None if S is None else S[0], self.recv2[0], P[0])

@@ -65,7 +65,8 @@ def _worker(rank, world, port, out):
         with open(out, "wb") as fh:
             pickle.dump(dict(U=torch.cat(parts).numpy(), W=torch.cat(wparts).numpy(), loss=loss.numpy(),
                              hist=res.fwd_hist, ahist=res.adj_hist, cyc=res.fwd_cycles,
-                             acyc=res.adj_cycles), fh)
+                             acyc=res.adj_cycles,
+                             fused=any(tr.ops.__dict__.get("_fused_cache", {}).values())), fh)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -87,23 +88,30 @@ def _single(rank, out):
                          W=d.stack.W.cpu().numpy(), loss=res.loss.cpu().numpy()), fh)
 
 
-def _spawn(fn, args, nprocs, out):
-    old = os.environ.get("LMG_NO_SWEEP")
-    os.environ["LMG_NO_SWEEP"] = "1"
+def _spawn(fn, args, nprocs, out, env=None):
+    """Run fn in nprocs spawned processes with `env` (default: the launch-per-step kernels,
+    LMG_NO_SWEEP=1) set for them; returns the pickle rank 0 wrote."""
+    env = {"LMG_NO_SWEEP": "1"} if env is None else env
+    keys = set(env) | {"LMG_NO_SWEEP"}
+    old = {k: os.environ.get(k) for k in keys}
+    for k in keys:
+        os.environ.pop(k, None)
+    os.environ.update(env)
     try:
         mp.spawn(fn, args=args, nprocs=nprocs, join=True)
     finally:
-        if old is None:
-            del os.environ["LMG_NO_SWEEP"]
-        else:
-            os.environ["LMG_NO_SWEEP"] = old
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
     with open(out, "rb") as fh:
         return pickle.load(fh)
 
 
-def _run(world, tmp_path):
+def _run(world, tmp_path, env=None):
     out = str(tmp_path / f"w{world}.pkl")
-    return _spawn(_worker, (world, _port(), out), world, out)
+    return _spawn(_worker, (world, _port(), out), world, out, env)
 
 
 def test_partitioned_training_step_bitwise_vs_single_gpu(tmp_path):
@@ -174,17 +182,27 @@ def test_partitioned_serial_baseline_matches_single_gpu(tmp_path):
     """LayerParallelTrainer.serial_step (the model-partitioned serial baseline of bench.py at
     N > 1) is bitwise the single-GPU sequential forward + sequential adjoint + SGD step with the
     launch-per-step kernels."""
-    old = os.environ.get("LMG_NO_SPLITK")
-    os.environ["LMG_NO_SPLITK"] = "1"  # one k-ascending chain everywhere (spawned processes)
-    try:
-        ref = _spawn(_serial_single, (str(tmp_path / "s1.pkl"),), 1, str(tmp_path / "s1.pkl"))
-        for world in (2, 4):
-            out = str(tmp_path / f"sw{world}.pkl")
-            r = _spawn(_serial_worker, (world, _port(), out), world, out)
-            assert r["W"].tobytes() == ref["W"].tobytes(), world
-            assert np.array_equal(r["loss"], ref["loss"]), world
-    finally:
-        if old is None:
-            del os.environ["LMG_NO_SPLITK"]
-        else:
-            os.environ["LMG_NO_SPLITK"] = old
+    env = {"LMG_NO_SWEEP": "1", "LMG_NO_SPLITK": "1"}  # one k-ascending chain everywhere
+    ref = _spawn(_serial_single, (str(tmp_path / "s1.pkl"),), 1, str(tmp_path / "s1.pkl"), env)
+    for world in (2, 4):
+        out = str(tmp_path / f"sw{world}.pkl")
+        r = _spawn(_serial_worker, (world, _port(), out), world, out, env)
+        assert r["W"].tobytes() == ref["W"].tobytes(), world
+        assert np.array_equal(r["loss"], ref["loss"]), world
+
+
+def test_partitioned_fused_fcf_bitwise(tmp_path):
+    """The layer-partitioned FCF as fused persistent sweeps (lmg_local_fcf_fused: halo chain,
+    exchange, block 0) against the single-GPU fused solve: with the one-chain sweep configuration
+    (LMG_SWEEP_CFG=0), forced on every level (LMG_SWEEP_ALL=1) and no split-K, states, histories
+    and updated parameters are BITWISE identical for world 1, 2 and 4."""
+    env = {"LMG_SWEEP_CFG": "0", "LMG_SWEEP_ALL": "1", "LMG_NO_SPLITK": "1"}
+    ref = _spawn(_single, (str(tmp_path / "f1.pkl"),), 1, str(tmp_path / "f1.pkl"), env)
+    for world in (1, 2, 4):
+        r = _run(world, tmp_path, env)
+        assert r["fused"], world  # the partitioned levels really ran lmg_local_fcf_fused
+        assert r["U"].tobytes() == ref["U"].tobytes(), world
+        assert np.array_equal(r["hist"], ref["hist"][: ref["cyc"].max() + 1], equal_nan=True), world
+        assert np.array_equal(r["ahist"], ref["ahist"][: ref["acyc"].max() + 1], equal_nan=True), world
+        assert r["W"].tobytes() == ref["W"].tobytes(), world
+        assert np.array_equal(r["loss"], ref["loss"]), world
