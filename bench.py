@@ -449,7 +449,9 @@ def run_ours(args, cfg):
         roofline=dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s",
                       frac=achieved / peak if peak else None,
                       traffic=traffic,
-                      kernel="lmg::step_gemm (FP64 DMMA m8n8k4, fused FAS epilogues): forward + adjoint layer steps",
+                      kernel="layer-step GEMM class, FP64 DMMA m8n8k4 with fused FAS epilogues: "
+                             "lmg::step_gemm (forward steps) + lmg::tgemm_kernel (warp-specialised "
+                             "TMA, adjoint steps); conv configs: lmg::conv_gemm",
                       peak_source="cuBLAS DGEMM 8192^3 measured in this run (FP64 is not in MEASURED_PEAKS.json)",
                       algorithmic="(2q^2+5q) flops per F-evaluation x B samples x tasks per launch",
                       share_of_step=(gemm_ms / (inst_ms * args.steps)) if inst_ms else None,
