@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "lmg.h"
@@ -426,8 +427,8 @@ bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr
 
 enum TileSel { SEL_AUTO = 0, SEL_SMALL = 1, SEL_WIDE = 2, SEL_TINY = 3, SEL_X1 = 4, SEL_X2 = 5 };
 // experimental shapes (LMG_TILE=x1|x2, fully tiled only), for tools/gemm_bench.py sweeps
-using TX1 = Tile<16, 64, 16, 1, 4, 4>;  // small batch: 4 warps of 16x16, 64 columns
-using TX2 = Tile<16, 32, 32, 1, 2, 3>;  // small batch: BK 32, half the k-tile barriers
+using TX1 = Tile<16, 32, 16, 1, 2, 3>;  // small batch: 3 stages (9 CTAs/SM)
+using TX2 = Tile<16, 32, 16, 1, 2, 6>;  // small batch: 6 stages (4 CTAs/SM, deeper per CTA)
 
 int tile_override() {
   static int v = [] {
@@ -561,6 +562,9 @@ bool is_conv(const lmg_system& s) { return s.kind == LMG_CONV || s.kind == LMG_C
 
 // ---- conv2d (lmg_conv.cuh) -------------------------------------------------------------------
 using CT = ConvTile<32, 64, 16, 2, 2, 4>;  // 32 pixels x 64 channels, warp 16x32
+// the adjoint stages two raster tiles (lambda and act'): 4 stages left it at 2 CTAs/SM (ncu:
+// DMMA pipe 44%, 2.41 ms per c3 sweep launch); 3 stages fit 3 CTAs/SM
+using CTA = ConvTile<32, 64, 16, 2, 2, 3>;
 
 ConvGeom geom_of(const lmg_system& S) {
   ConvGeom g;
@@ -576,21 +580,23 @@ ConvGeom geom_of(const lmg_system& S) {
 
 template <int V>
 int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
-  constexpr int A_SZ = CT::BK * CT::LDA;
-  constexpr int B_SZ = (V == CV_ADJ) ? CT::BN * CT::LDB_K : CT::BK * CT::LDB_MN;
+  using T = typename std::conditional<V == CV_ADJ, CTA, CT>::type;
+  static_assert(T::BM == CT::BM && T::BN == CT::BN, "geometry padding assumes CT's tile");
+  constexpr int A_SZ = T::BK * T::LDA;
+  constexpr int B_SZ = (V == CV_ADJ) ? T::BN * T::LDB_K : T::BK * T::LDB_MN;
   constexpr int STAGE = A_SZ * (V == CV_ADJ ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
-  constexpr size_t SMEM = (size_t)CT::STAGES * STAGE * sizeof(double);
-  auto kern = conv_gemm<CT, V>;
+  constexpr size_t SMEM = (size_t)T::STAGES * STAGE * sizeof(double);
+  auto kern = conv_gemm<T, V>;
   static const cudaError_t attr =
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
   if (attr != cudaSuccess) return fail(LMG_ERR_CUDA, cudaGetErrorString(attr));
   if (a.ntasks > 65535) return fail(LMG_ERR_CONFIGURATION, "too many tasks in one launch");
-  dim3 grid((a.N + CT::BN - 1) / CT::BN, (a.M + CT::BM - 1) / CT::BM, a.ntasks);
+  dim3 grid((a.N + T::BN - 1) / T::BN, (a.M + T::BM - 1) / T::BM, a.ntasks);
   const int cls = V == CV_FWD ? CLS_GEMM_FWD : (V == CV_ADJ ? CLS_GEMM_ADJ : CLS_GEMM_PG);
   // algorithmic: 2 * 9 C^2 per pixel per sample (zero padding counted as work, kernels.py:135)
   const double flops = (double)a.ntasks * 2.0 * 9.0 * g.C * g.C * (double)g.HW *
                        (V == CV_PGRAD ? (double)(a.K / g.HWp) : (double)(a.M / g.HWp));
-  return launch(cls, flops, 0.0, st, [&] { kern<<<grid, CT::NT, SMEM, st>>>(a, g); });
+  return launch(cls, flops, 0.0, st, [&] { kern<<<grid, T::NT, SMEM, st>>>(a, g); });
 }
 
 // residual partial slots per state row (one per CTA tile of a row, canonical per tile config)
