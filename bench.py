@@ -188,6 +188,11 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        """Start polling and wait for the first sample, so nvidia-smi's start-up (NVML init) is
+        not inside the timed region (it measurably stalled short, sync-heavy steps like c5)."""
+        import threading
+
+        self.lines, self._warm = [], 0
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
@@ -195,13 +200,31 @@ class ClockSampler:
                 stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return self
+        first = threading.Event()
+
+        def reader():
+            for ln in self.proc.stdout:
+                self.lines.append(ln)
+                first.set()
+
+        self._thread = threading.Thread(target=reader, daemon=True)
+        self._thread.start()
+        first.wait(timeout=10.0)
+        self._warm = len(self.lines)  # samples taken before the timed region
         return self
 
     def __exit__(self, *exc):
         if self.proc is not None:
             self.proc.terminate()
-            out, _ = self.proc.communicate(timeout=10)
-            self.lines = out.strip().splitlines()
+            try:
+                self.proc.wait(timeout=10)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self._thread.join(timeout=5)
+            # the last pre-region sample stands in when the region was shorter than one period
+            keep = self.lines[self._warm:] or self.lines[-1:]
+            self.lines = [ln.strip() for ln in keep]
         else:
             self.lines = []
 

@@ -425,10 +425,10 @@ int n_tiles(int N) { return (N + TSmall::BN - 1) / TSmall::BN; }
 
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-enum TileSel { SEL_AUTO = 0, SEL_SMALL = 1, SEL_WIDE = 2, SEL_TINY = 3, SEL_X1 = 4, SEL_X2 = 5 };
-// experimental shapes (LMG_TILE=x1|x2, fully tiled only), for tools/gemm_bench.py sweeps
-using TX1 = Tile<16, 32, 16, 1, 2, 3>;  // small batch: 3 stages (9 CTAs/SM)
-using TX2 = Tile<16, 32, 16, 1, 2, 6>;  // small batch: 6 stages (4 CTAs/SM, deeper per CTA)
+enum TileSel { SEL_AUTO = 0, SEL_SMALL = 1, SEL_WIDE = 2, SEL_TINY = 3 };
+// Shapes measured and not kept (tools/gemm_bench.py, tools/sweep_bench.py): 32x32 BK 32 (26.6 vs
+// 28.0 TF/s at c2), 64x32 8 warps (27.8); small batch 16x64 4 warps (= TTiny), 16x32 BK 32
+// (-5%), 16x32 3 / 6 stages (+1% / -3% at c5).
 
 int tile_override() {
   static int v = [] {
@@ -436,8 +436,6 @@ int tile_override() {
     if (e && !strcmp(e, "small")) return (int)SEL_SMALL;
     if (e && !strcmp(e, "wide")) return (int)SEL_WIDE;
     if (e && !strcmp(e, "tiny")) return (int)SEL_TINY;
-    if (e && !strcmp(e, "x1")) return (int)SEL_X1;
-    if (e && !strcmp(e, "x2")) return (int)SEL_X2;
     return (int)SEL_AUTO;
   }();
   return v;
@@ -465,8 +463,6 @@ int launch_layout(const StepArgs& a, bool v2, cudaStream_t st) {
     return a.M % BM == 0 && a.N % BN == 0 && a.K % BK == 0 && !getenv("LMG_NO_FULL");
   };
   const int sel = choose_tile<AK, BKM, ASC>(a);
-  if (sel == SEL_X1 && full(TX1::BM, TX1::BN, TX1::BK)) return launch_cfg<TX1, AK, BKM, ASC, 2, true>(a, st);
-  if (sel == SEL_X2 && full(TX2::BM, TX2::BN, TX2::BK)) return launch_cfg<TX2, AK, BKM, ASC, 2, true>(a, st);
   if (sel == SEL_TINY) {
     if (full(TTiny::BM, TTiny::BN, TTiny::BK)) return launch_cfg<TTiny, AK, BKM, ASC, 2, true>(a, st);
     return launch_cfg<TTiny, AK, BKM, ASC, 2>(a, st);
