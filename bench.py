@@ -41,6 +41,11 @@ CONFIGS = {
                workload="conv ResNet 256 layers (3x3 conv+bias+ReLU, 64 ch, 32x32) batch 32, 3-level "
                         "FAS (cf 4, levels [256,64,16]) forward+adjoint training step to tol 1e-9; "
                         "dense tanh opening from 64 features"),
+    # BASELINE.json configs[3]: deep dense ResNet, layer-partitioned across 2/4/8 GPUs (SURVEY 8d:
+    # cf 4, 2 levels [4096, 1024]); theta 32 GiB, states 32 GiB -- it also fits one B200
+    "c4": dict(depth=4096, width=1024, batch=1024, cf=4, threshold=1024, tol=1e-9, max_cycles=50,
+               lr=0.1, workload="dense tanh ResNet 4096 layers width 1024 batch 1024, 2-level FAS "
+                                "(cf 4, levels [4096,1024]) forward+adjoint training step to tol 1e-9"),
     # configs[4]-style HBM-bound point (q=512, B=16, cf 16)
     "c5": dict(depth=1024, width=512, batch=16, cf=16, threshold=4, tol=1e-9, max_cycles=50, lr=0.1,
                workload="dense tanh ResNet 1024 layers width 512 batch 16, 3-level FAS cf 16 "
@@ -60,6 +65,8 @@ def parse():
     p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     p.add_argument("--adjoint", default="fas", choices=["fas", "sequential"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--batch", type=int, default=None,
+                   help="override the config's batch (functional checks; recorded in config)")
     p.add_argument("--split", type=int, default=None,
                    help="batch slices on concurrent streams (default: 2 when B >= 64)")
     return p.parse_args()
@@ -463,7 +470,11 @@ def run_ours(args, cfg):
                     threshold=cfg["threshold"], tol=cfg["tol"], adjoint=args.adjoint,
                     parallelism=(f"layer-partitioned x{world}" if world > 1 else
                                  f"single GPU, {getattr(tr, 'split', 1)} batch slice(s) on concurrent streams"),
-                    l2="inputs larger than L2 (theta 2 GiB, states 1 GiB), no flush",
+                    l2=(f"inputs larger than L2 (theta {N * q * q * 8 / 2**30:.2f} GiB, states "
+                        f"{N * B * q * 8 / 2**30:.2f} GiB), no flush"
+                        if N * q * q * 8 > 2 * 126e6 else
+                        "theta smaller than L2: cycles re-read it from L2 (no flush; the FAS step "
+                        "is latency-bound at this size)"),
                     cycles_per_step=cycles),
         e2e=dict(value=N * B / (e2e_ms * 1e-3), unit=UNIT,
                  h2d_bytes_per_step=int(X_host.numel() * 8 + lab_host.numel() * 8),
@@ -509,7 +520,15 @@ def run_ours(args, cfg):
 
 def main():
     args = parse()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.batch is not None:
+        cfg["batch"] = args.batch
+        cfg["workload"] += f" [batch overridden to {args.batch}]"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config == "c4" and world == 1 and cfg["batch"] == 1024 and args.impl != "reference":
+        raise SystemExit("c4 (4096 x 1024, batch 1024) needs >= 2 GPUs: theta 32 GiB + states, "
+                         "adjoint and act' 3 x 32 GiB + level-0 workspace exceed one B200; run it "
+                         "layer-partitioned (torchrun --nproc-per-node 2..8) or with --batch 512")
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
