@@ -530,17 +530,16 @@ int launch_step(Layout L, const StepArgs& a, cudaStream_t st) {
   if (L == L_FWD) v2 = v2 && (a.K % 2 == 0);
   if (L == L_ADJ) v2 = v2 && (a.K % 2 == 0) && (a.N % 2 == 0);
   if (L == L_PG) v2 = v2 && (a.M % 2 == 0) && (a.N % 2 == 0);
-  if (L != L_PG && v2 && tgemm_eligible(a, L == L_ADJ)) {
+  TgPlan* plan = nullptr;
+  if (L != L_PG && v2 && tgemm_prepare(a, L == L_ADJ, &plan)) {
     // big-batch steps: the warp-specialised TMA kernel (lmg_tgemm.cu), bitwise the same math
     const int cls = L == L_FWD ? CLS_GEMM_FWD : CLS_GEMM_ADJ;
     const double flops = (double)a.ntasks * ((double)a.M * a.N * (2.0 * a.K + 5.0));
     const double bytes = 8.0 * a.ntasks * ((double)a.N * a.K + (double)a.M * a.K + 2.0 * a.M * a.N);
-    bool launched = false;
     cudaError_t e = cudaSuccess;
-    TRY(launch(cls, flops, bytes, st, [&] { e = tgemm_launch(a, L == L_ADJ, st, &launched); }));
+    TRY(launch(cls, flops, bytes, st, [&] { e = tgemm_launch(plan, L == L_ADJ, st); }));
     if (e != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("tgemm: ") + cudaGetErrorString(e));
-    if (launched) return LMG_OK;
-    g_launches--;  // nothing was launched: fall through to step_gemm
+    return LMG_OK;
   }
   switch (L) {
     case L_FWD: return launch_layout<true, true, false>(a, v2, st);

@@ -277,35 +277,51 @@ int tile_kind(const StepArgs& a, bool adj) {  // 0: none, 1: big, 2: small
 }
 }  // namespace
 
-int tgemm_eligible(const StepArgs& a, bool adj) { return tile_kind(a, adj) != 0; }
-
-cudaError_t tgemm_launch(const StepArgs& a, bool adj, cudaStream_t st, bool* launched) {
-  *launched = false;
-  const int kind = tile_kind(a, adj);
-  if (!kind) return cudaSuccess;
-  const int BM = kind == 1 ? 64 : 16, BN = kind == 1 ? 64 : 32;
-  if ((int64_t)a.ntasks * (a.M / BM) * (a.N / BN) >= ((int64_t)1 << 31)) return cudaSuccess;
+struct TgPlan {
   TgParams prm;
+  int kind = 0;
+};
+
+bool tgemm_prepare(const StepArgs& a, bool adj, TgPlan** plan) {
+  *plan = nullptr;
+  const int kind = tile_kind(a, adj);
+  if (!kind) return false;
+  const int BM = kind == 1 ? 64 : 16, BN = kind == 1 ? 64 : 32;
+  if ((int64_t)a.ntasks * (a.M / BM) * (a.N / BN) >= ((int64_t)1 << 31)) return false;
+  TgPlan* pl = new TgPlan;
+  TgParams& prm = pl->prm;
   prm.a = a;
   prm.mtiles = a.M / BM;
   prm.ntiles = a.N / BN;
   prm.ntiles_total = a.ntasks * prm.mtiles * prm.ntiles;
   // A: rows m of task t (K-major, lda); W: forward rows n (K-major, ldb), adjoint rows k (ldb)
-  if (!make_map(&prm.amap, &prm.a_row0, &prm.a_rowts, a.A, a.A_ts, a.ntasks, a.M, a.lda, 4, BM, false))
-    return cudaSuccess;
-  if (!make_map(&prm.bmap, &prm.b_row0, &prm.b_rowts, a.Bm, a.B_ts, a.ntasks, adj ? a.K : a.N, a.ldb,
-                4, adj ? TBK : BN, false))
-    return cudaSuccess;
-  if (adj && !make_map(&prm.dmap, &prm.d_row0, &prm.d_rowts, a.Ds, a.Ds_ts, a.ntasks, a.M, a.lda, 4,
-                       BM, false))
-    return cudaSuccess;
+  bool ok = make_map(&prm.amap, &prm.a_row0, &prm.a_rowts, a.A, a.A_ts, a.ntasks, a.M, a.lda, 4, BM, false) &&
+            make_map(&prm.bmap, &prm.b_row0, &prm.b_rowts, a.Bm, a.B_ts, a.ntasks, adj ? a.K : a.N, a.ldb,
+                     4, adj ? TBK : BN, false);
+  if (ok && adj)
+    ok = make_map(&prm.dmap, &prm.d_row0, &prm.d_rowts, a.Ds, a.Ds_ts, a.ntasks, a.M, a.lda, 4, BM, false);
+  if (!ok) {
+    delete pl;
+    return false;
+  }
   if (!adj) {
     prm.d_row0 = prm.d_rowts = 0;
     prm.dmap = prm.amap;
   }
-  *launched = true;
-  if (kind == 1) return adj ? launch_t<TBigA>(prm, st) : launch_t<TBig>(prm, st);
-  return adj ? launch_t<TSmA>(prm, st) : launch_t<TSm>(prm, st);
+  pl->kind = kind;
+  *plan = pl;
+  return true;
+}
+
+cudaError_t tgemm_launch(TgPlan* plan, bool adj, cudaStream_t st) {
+  TgParams& prm = plan->prm;
+  cudaError_t e;
+  if (plan->kind == 1)
+    e = adj ? launch_t<TBigA>(prm, st) : launch_t<TBig>(prm, st);
+  else
+    e = adj ? launch_t<TSmA>(prm, st) : launch_t<TSm>(prm, st);
+  delete plan;
+  return e;
 }
 
 }  // namespace lmg

@@ -7,10 +7,11 @@
 
 namespace lmg {
 
-// 1 if the TMA kernel can run this launch (64 x 64 tiles, no E_RESID / E_PGRAD)
-int tgemm_eligible(const StepArgs& a, bool adj);
-// launches it; *launched = false (and cudaSuccess) if an operand cannot be described by a
-// tensor map, so the caller falls back to step_gemm
-cudaError_t tgemm_launch(const StepArgs& a, bool adj, cudaStream_t st, bool* launched);
+struct TgPlan;
+// builds the launch (tensor maps) if the TMA kernel applies to this step (64 x 64 tiles on the
+// adjoint layout by default, no E_RESID / E_PGRAD) and every operand is describable; else false
+bool tgemm_prepare(const StepArgs& a, bool adj, TgPlan** plan);
+// launches a prepared plan and frees it
+cudaError_t tgemm_launch(TgPlan* plan, bool adj, cudaStream_t st);
 
 }  // namespace lmg
