@@ -8,8 +8,12 @@ then an equal split) and the matching rows of the coarsest level.  Per cycle and
   after FCF part A : U[L]            1 row   (the reference's one BoundaryMessage per edge per
                                               C-sweep, parallel.py:183-216)
   after FCF part B : P[nb], adv_out  2 rows  (C-row residual and coarse-source halo)
-  coarsest level   : the exact forward substitution is rank-pipelined: each rank solves its rows
-                     and hands its last state to the next (1 row); no theta or grid gather
+  coarsest level   : gathered (default, north_star / SURVEY 8e): S_H rows, and once per solve the
+                     coarse theta (+ act' rows for the adjoint), are all-gathered; every rank
+                     runs the same exact forward substitution of the whole coarse grid and keeps
+                     its rows (the scatter becomes local slicing).  LMG_COARSEST=pipeline: each
+                     rank solves its rows and hands its last state to the next (1 row per edge,
+                     no theta replication).
   norms            : all_gather of per-block partials (B doubles per block), summed in global
                      block order -> bitwise the single-GPU norms.
 
@@ -152,8 +156,19 @@ class DistSolver:
     """FAS solve of a layer-partitioned system (forward or adjoint) on this rank."""
 
     def __init__(self, view_local, N_total, c, nlevels, B, *, rank, world, ops, reverse=False,
-                 adjoint_D=None, device=None, group=None):
+                 adjoint_D=None, device=None, group=None, coarsest=None):
+        import os
+
         import torch.distributed as dist
+
+        # coarsest-level exact solve: "gather" (north_star / SURVEY 8e: S_H and the coarse theta
+        # gathered to the first rank, one serial solve there, V scattered back) or "pipeline"
+        # (each rank solves its rows and hands its last state on; no theta replication)
+        mode = coarsest or os.environ.get("LMG_COARSEST") or ("gather" if ops.name == "cuda" else "pipeline")
+        if mode not in ("gather", "pipeline"):
+            raise ConfigurationError(f"coarsest must be 'gather' or 'pipeline', got {mode!r}")
+        self.coarsest_mode = mode
+        self._gsys = None
 
         self.dist = dist
         self.group = group
@@ -258,6 +273,8 @@ class DistSolver:
 
     # -- rank-pipelined exact solve of the coarsest level (network.py:111-123) ----------------
     def _coarsest(self, l, V, SH):
+        if self.coarsest_mode == "gather" and self.world > 1:
+            return self._coarsest_gather(l, V, SH)
         lev = self.levels[l]
         ops = self.ops
         if self.is_first:
@@ -270,6 +287,73 @@ class DistSolver:
         if self.has_next:
             ops.adv_last(lev, V, self.recv2[0:1])
             self._exchange(self.recv2[0:1], None)
+
+    # -- the gathered coarsest solve ------------------------------------------
+    def _allgather(self, x):
+        """all_gather along dim 0 in RANK order (host-staged under gloo)."""
+        dist, t = self.dist, self.t
+        if self._host_staged():
+            loc = x.contiguous().cpu()
+            parts = [t.empty_like(loc) for _ in range(self.world)]
+            dist.all_gather(parts, loc, group=self.group)
+            return t.cat(parts, 0).to(x.device)
+        parts = [t.empty_like(x) for _ in range(self.world)]
+        dist.all_gather(parts, x.contiguous(), group=self.group)
+        return t.cat(parts, 0)
+
+    def _global_coarse_system(self, l):
+        """The coarsest level of the whole system on every rank, gathered once per solve (theta
+        changes only between steps): its blocks in SYSTEM order -- forward: each rank's local
+        layers j*s in rank order; adjoint (reversed system, multigrid.py:101 applied to it): each
+        rank's local layers L-1-j*s, ranks in reverse order -- plus the adjoint's act' rows."""
+        import ctypes
+
+        if self._gsys is not None:
+            return self._gsys
+        t = self.t
+        lev = self.levels[l]
+        view = lev.view
+        st = view.stack
+        n, s = lev.L, view.stride
+        adj = lev.adjoint_D is not None
+        base = st.num_blocks - 1 if adj else 0
+        idx = t.arange(n, device=st.W.device) * (-s if adj else s) + base
+        order = range(self.world - 1, -1, -1) if self.reverse else range(self.world)
+
+        def gathered(x):
+            parts = self._allgather(x).view(self.world, *x.shape)
+            return t.cat([parts[r] for r in order], 0).contiguous()
+
+        Wg = gathered(st.W.index_select(0, idx))
+        bg = None if adj else gathered(st.b.index_select(0, idx))
+        Dg = gathered(lev.adjoint_D.index_select(0, idx)) if adj else None
+        loc = lev.desc()
+        d = _lib.LmgSystem()
+        ctypes.memmove(ctypes.byref(d), ctypes.byref(loc), ctypes.sizeof(d))  # kind, act, step, geometry
+        d.num_layers = n * self.world
+        d.W, d.w_stride = Wg.data_ptr(), Wg[0].numel()
+        if adj:
+            d.b, d.b_stride = None, 0
+            d.D, d.d_stride = Dg.data_ptr(), Dg[0].numel()
+        else:
+            d.b, d.b_stride = bg.data_ptr(), bg[0].numel()
+        self._gsys = (Wg, bg, Dg, d)  # keep the gathered tensors alive with the descriptor
+        return self._gsys
+
+    def _coarsest_gather(self, l, V, SH):
+        lev = self.levels[l]
+        n, t = lev.L, self.t
+        desc = self._global_coarse_system(l)[3]
+        # S_H rows in SYSTEM order: rank order forward, reversed rank order for the adjoint
+        parts = self._allgather(SH[:n]).view(self.world, n, self.B, lev.q)
+        order = range(self.world - 1, -1, -1) if self.reverse else range(self.world)
+        SHg = t.cat([parts[r] for r in order], 0)
+        Vg = t.empty_like(SHg)
+        # every rank runs the same serial solve (the first rank's result is what the reference's
+        # single process computes; running it everywhere replaces the scatter by local slicing)
+        _lib.call("lmg_sequential_forward", desc, self.B, SHg.data_ptr(), _lib.SRC_DENSE,
+                  Vg.data_ptr(), self.ops._st())
+        V[:n].copy_(Vg[self.pos * n : (self.pos + 1) * n])
 
     # -- one FAS cycle at level l (multigrid.py:175-228) --------------------------------------
     def cycle(self, l, U, S, smode, want_norm):
@@ -326,6 +410,7 @@ class DistSolver:
         L = self.levels[0].L
         if hasattr(self.ops, "bind_stream"):
             self.ops.bind_stream()
+        self._gsys = None  # parameters may have changed since the last solve (SGD)
         if not use_initial:
             if self.is_first:
                 U0[:L].copy_(S0[0] if smode == _lib.SRC_DENSE else S0)

@@ -114,7 +114,8 @@ def _run(world, tmp_path, env=None):
     return _spawn(_worker, (world, _port(), out), world, out, env)
 
 
-def test_partitioned_training_step_bitwise_vs_single_gpu(tmp_path):
+@pytest.mark.parametrize("coarsest", ["gather", "pipeline"])
+def test_partitioned_training_step_bitwise_vs_single_gpu(tmp_path, coarsest):
     import paper_2007_07336_b200 as P
 
     X, labels = _inputs()
@@ -131,7 +132,7 @@ def test_partitioned_training_step_bitwise_vs_single_gpu(tmp_path):
     assert np.max(np.abs(ref["U"] - U)) <= 1e-12 * max(1.0, np.max(np.abs(U)))
     assert np.max(np.abs(ref["W"] - W1)) <= 1e-12 * max(1.0, np.max(np.abs(W1)))
     for world in (1, 2, 4):
-        r = _run(world, tmp_path)
+        r = _run(world, tmp_path, {"LMG_NO_SWEEP": "1", "LMG_COARSEST": coarsest})
         assert r["U"].tobytes() == ref["U"].tobytes(), world
         assert np.array_equal(r["hist"], ref["hist"][: ref["cyc"].max() + 1], equal_nan=True), world
         assert np.array_equal(r["ahist"], ref["ahist"][: ref["acyc"].max() + 1], equal_nan=True), world
