@@ -200,6 +200,9 @@ class ClockSampler:
         import threading
 
         self.lines, self._warm = [], 0
+        if os.environ.get("LMG_BENCH_NO_CLOCKS"):  # diagnosis only: no sampler at all
+            self.proc = None
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
