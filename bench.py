@@ -162,7 +162,7 @@ def run_reference(args, cfg):
     times, vals = [], []
     info = None
     # the number of forward cycles the solve needs at this config (c2: 36)
-    cyc = {"c2": 36, "c1": 7, "c5": 8, "c3": 16}[args.config]
+    cyc = {"c2": 36, "c1": 7, "c5": 8, "c3": 16, "c4": 6}[args.config]  # measured on B200
     for i in range(args.warmup + args.steps):
         v, info = cpu_reference_sample(cfg, cyc)
         if i >= args.warmup:
