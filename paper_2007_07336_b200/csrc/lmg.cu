@@ -865,16 +865,13 @@ SweepArgs local_fused_args(const lmg_system& S, int B, int c, double* U, const d
 
 bool local_fused_ok(const lmg_system& S, int B, int c, bool is_first, bool has_next) {
   if (B > sweep_max_batch() || !sweep_basic_ok(S) || S.num_layers % c) return false;
-  const int nb = S.num_layers / c;
   SweepArgs a = local_fused_args(S, B, c, nullptr, nullptr, LMG_SRC_HEAD, is_first, has_next,
                                  nullptr, nullptr, nullptr, nullptr, 0);
   if (a.nchains <= 0) a.nchains = 1;
   SweepShape sh;
   if (sweep_shape(a, &sh) < 0) return false;
   static const bool all = getenv("LMG_SWEEP_ALL") != nullptr;
-  if (!all && (int)(sh.grid.y * sh.grid.z) > sweep_clusters(S.width, a.adj, sh.cfg)) return false;
-  (void)nb;
-  return true;
+  return all || (int)(sh.grid.y * sh.grid.z) <= sweep_clusters(S.width, a.adj, sh.cfg);
 }
 
 int local_fcf_fused(const lmg_system& S, int B, int c, double* U, const double* src, int mode,

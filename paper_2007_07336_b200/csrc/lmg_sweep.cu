@@ -413,14 +413,13 @@ template <class C>
 cudaError_t make_params(const SweepArgs& a, SweepParams* p) {
   EncodeTiled enc = encoder();
   if (!enc) return cudaErrorNotSupported;
-  const int64_t q = a.q, q2 = q * q;
+  const int64_t q = a.q;
   const int64_t span = (int64_t)(a.n - 1) * a.w_stride;  // may be negative (adjoint)
   const double* base = span < 0 ? a.W + span : a.W;
   p->a = a;
   p->row_stride = a.w_stride / q;
   p->row_off = (a.W - base) / q;
   const cuuint64_t rows = (cuuint64_t)((span < 0 ? -span : span) / q + q);
-  (void)q2;
   cuuint64_t dims[2] = {(cuuint64_t)q, rows};
   cuuint64_t strides[1] = {(cuuint64_t)q * 8};
   cuuint32_t box[2], estr[2] = {1, 1};
