@@ -794,8 +794,15 @@ int seq_sweep(const lmg_system& S, int B, const double* src, int mode, double* U
   // one wave of clusters only (cudaOccupancyMaxActiveClusters: at q = 512 on B200, 7 clusters of
   // 16 CTAs or 15 of 8): beyond that the split-K per-step path measured faster (B = 256, 64
   // steps: 12.4 vs 18.7 us per step with 8-CTA clusters in two waves)
-  if ((int)sh.grid.y > sweep_clusters(S.width, a.adj, sh.cfg) && sh.cfg == 1)
-    if (sweep_shape(a, &sh, 0) < 0) return -1;
+  // wider CTAs (smaller clusters) until every batch tile's chain is resident at once.  The
+  // 128-column / 4-CTA shape (cfg 2) also fits B = 256 in one wave but measured no faster than
+  // the split-K path under graph replay (c2: 1076 vs 1071 ms per step), so it is opt-in
+  // (LMG_SWEEP_CFG=2)
+  for (int cfg : {0}) {
+    if ((int)sh.grid.y <= sweep_clusters(S.width, a.adj, sh.cfg)) break;
+    SweepShape alt;
+    if (sweep_shape(a, &alt, cfg) == 0 && alt.cfg == cfg) sh = alt;
+  }
   if ((int)sh.grid.y > sweep_clusters(S.width, a.adj, sh.cfg)) return -1;
   const int64_t BQ = (int64_t)B * S.width;
   TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]

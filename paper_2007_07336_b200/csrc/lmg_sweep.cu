@@ -45,9 +45,9 @@ namespace cg = cooperative_groups;
 constexpr int SW_BM = 16;  // batch rows per chain tile (two m8 fragments)
 constexpr int SMEM_MAX = 232448;
 
-template <int NC_, int KS_, int ST_, bool ADJ_>
+template <int NC_, int KS_, int ST_, bool ADJ_, int BK_ = 32>
 struct SwCfg {
-  static constexpr int NC = NC_, KS = KS_, BK = 32, ST = ST_;
+  static constexpr int NC = NC_, KS = KS_, BK = BK_, ST = ST_;
   static constexpr bool ADJ = ADJ_;
   static constexpr int MT = SW_BM / 8;
   static constexpr int NFG = NC / 8;        // 8-column fragment groups (one per warp, per k-split)
@@ -384,6 +384,21 @@ using Cfg64F = SwCfg<64, 1, 5, false>;
 using Cfg32F = SwCfg<32, 2, 7, false>;
 using Cfg64A = SwCfg<64, 1, 5, true>;
 using Cfg32A = SwCfg<32, 2, 7, true>;
+// 128 columns per CTA (cluster q/128, 16 DMMA warps, 16-k stages): for serial solves of many
+// batch tiles -- at q = 512 only 15 eight-CTA clusters are co-resident, so B = 256 (16 tiles)
+// needs the 4-CTA clusters to stay in one wave
+using Cfg128F = SwCfg<128, 1, 5, false, 16>;
+using Cfg128A = SwCfg<128, 1, 4, true, 16>;
+
+// run f with the configuration tag of (cfg, adjoint)
+template <class F>
+auto with_cfg(int cfg, bool adj, F&& f) {
+  switch (cfg) {
+    case 0: return adj ? f(Cfg64A{}) : f(Cfg64F{});
+    case 1: return adj ? f(Cfg32A{}) : f(Cfg32F{});
+    default: return adj ? f(Cfg128A{}) : f(Cfg128F{});
+  }
+}
 
 typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -488,22 +503,26 @@ int sweep_shape(const SweepArgs& a, SweepShape* s, int forced_cfg) {
   const int nchains = a.mode == SW_SEQ ? 1 : (a.nchains > 0 ? a.nchains : a.n / a.c);
   const int mt = (a.B + SW_BM - 1) / SW_BM;
   int cfg = sweep_config(a.q, a.B, a.adj, nchains);
-  if (forced_cfg == 0 && (a.adj ? fits<Cfg64A>(a.q) : fits<Cfg64F>(a.q))) cfg = 0;
-  if (forced_cfg == 1 && (a.adj ? fits<Cfg32A>(a.q) : fits<Cfg32F>(a.q))) cfg = 1;
+  if (forced_cfg >= 0) {
+    const bool ok = with_cfg(forced_cfg, a.adj, [&](auto c) { return fits<decltype(c)>(a.q); });
+    if (ok) cfg = forced_cfg;
+    else if (forced_cfg == 2) return -1;
+  }
   if (cfg < 0) return -1;
-  const int NC = cfg == 0 ? 64 : 32;
   s->cfg = cfg;
-  s->cs = a.q / NC;
-  s->nthreads = 9 * 32;
-  s->smem = cfg == 0 ? (a.adj ? Cfg64A::smem(a.q) : Cfg64F::smem(a.q))
-                     : (a.adj ? Cfg32A::smem(a.q) : Cfg32F::smem(a.q));
+  with_cfg(cfg, a.adj, [&](auto c) {
+    using C = decltype(c);
+    s->cs = a.q / C::NC;
+    s->nthreads = C::NT;
+    s->smem = C::smem(a.q);
+    return 0;
+  });
   s->grid = dim3(s->cs, mt, nchains);
   return 0;
 }
 
 cudaError_t sweep_launch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
-  if (s.cfg == 0) return a.adj ? launch_c<Cfg64A>(a, s, st) : launch_c<Cfg64F>(a, s, st);
-  return a.adj ? launch_c<Cfg32A>(a, s, st) : launch_c<Cfg32F>(a, s, st);
+  return with_cfg(s.cfg, a.adj, [&](auto c) { return launch_c<decltype(c)>(a, s, st); });
 }
 
 // how many clusters of a configuration can be co-resident (cudaOccupancyMaxActiveClusters)
@@ -511,7 +530,7 @@ int sweep_max_clusters(int q, int adj, int cfg) {
   SweepArgs a{};
   a.mode = SW_SEQ; a.B = 16; a.q = q; a.n = 2; a.adj = adj;
   SweepShape sh;
-  if (sweep_shape(a, &sh, cfg) < 0) return -1;
+  if (sweep_shape(a, &sh, cfg) < 0 || sh.cfg != cfg) return -1;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(sh.cs, 64, 1);
   lc.blockDim = dim3(sh.nthreads, 1, 1);
@@ -524,18 +543,12 @@ int sweep_max_clusters(int q, int adj, int cfg) {
   lc.attrs = at;
   lc.numAttrs = 1;
   int n = -1;
-  cudaError_t e;
-  if (sh.cfg == 0) {
-    auto k = adj ? sweep_kernel<Cfg64A> : sweep_kernel<Cfg64F>;
+  const cudaError_t e = with_cfg(cfg, adj, [&](auto c) {
+    auto k = sweep_kernel<decltype(c)>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
     cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    e = cudaOccupancyMaxActiveClusters(&n, k, &lc);
-  } else {
-    auto k = adj ? sweep_kernel<Cfg32A> : sweep_kernel<Cfg32F>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
-    cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    e = cudaOccupancyMaxActiveClusters(&n, k, &lc);
-  }
+    return cudaOccupancyMaxActiveClusters(&n, k, &lc);
+  });
   return e == cudaSuccess ? n : -(int)e;
 }
 

@@ -28,6 +28,7 @@ CASES = [
     (128, 256, 20, 4, 8),    # two batch tiles (20 = 16 + 4 masked rows), 3 levels
     (96, 64, 33, 2, 12),     # cf 2, three batch tiles, 4 levels [96,48,24,12]
     (64, 512, 160, 4, 16),   # B > 64: per-step FCF, serial coarsest solve on 10 batch tiles
+    (64, 512, 256, 4, 16),   # 16 batch tiles: serial solves on 4-CTA clusters (128 columns)
     (128, 128, 12, 4, 8, "relu"),      # the other fused activations
     (64, 256, 16, 4, 0, "identity"),
 ]
