@@ -495,6 +495,7 @@ int sweep_config(int q, int B, int adj, int nchains) {
   const bool ok32 = adj ? fits<Cfg32A>(q) : fits<Cfg32F>(q);
   if (forced == 0 && ok64) return 0;
   if (forced == 1 && ok32) return 1;
+  if (forced == 2 && (adj ? fits<Cfg128A>(q) : fits<Cfg128F>(q))) return 2;
   if (nchains > 16 && ok64) return 0;
   return ok32 ? 1 : (ok64 ? 0 : -1);
 }

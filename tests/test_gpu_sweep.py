@@ -60,6 +60,16 @@ def test_fused_sweep_matches_per_step(case, tmp_path):
         assert on[key].shape == off[key].shape, key
         assert _close(on[key], off[key], rel), (key, float(np.nanmax(np.abs(on[key] - off[key]))))
     assert int(on["launches"]) <= int(off["launches"])  # B > 144: no fused launch applies
+    # the other shapes, forced: 32 columns / 16-CTA clusters (k split over warp pairs) and
+    # 128 columns / 4-CTA clusters (serial solves of many batch tiles)
+    forced = ["1"] + (["2"] if case[1] % 128 == 0 and case[1] <= 512 else [])
+    for cfg in forced:
+        f = _run(case, tmp_path, {"LMG_SWEEP_CFG": cfg})
+        for key in ("cyc", "adj_cyc"):
+            assert np.array_equal(f[key], off[key]), (cfg, key)
+        for key, rel in (("U1", 1e-12), ("lam", 1e-12), ("W", 1e-12), ("Us", 1e-12),
+                         ("hist", 1e-9), ("adj_hist", 1e-9)):
+            assert _close(f[key], off[key], rel), (cfg, key)
     if case[1] % 64 == 0:  # one-chain configuration: bitwise (the serial split-K path is not)
         one = _run(case, tmp_path, {"LMG_SWEEP_CFG": "0", "LMG_NO_SPLITK": "1"})
         off = _run(case, tmp_path, {"LMG_NO_SWEEP": "1", "LMG_NO_SPLITK": "1"})  # one chain too
