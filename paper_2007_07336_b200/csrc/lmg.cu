@@ -1002,14 +1002,19 @@ int local_fcf_a(const lmg_system& S, int B, int c, double* U, const double* src,
   int s0 = 0;
   if (Q && c > 1) {
     // rows kc+1 = propagate(U[kc]) were produced by the previous cycle's residual (Q) from the
-    // same, unchanged U[kc]: copy instead of recomputing (bitwise identical)
-    TRY(copy_rows(U + BQ, c * BQ, Q, BQ, K1, BQ, st));
+    // same, unchanged U[kc]: reuse instead of recomputing (bitwise identical).  For c > 2 the row
+    // is only the next F step's input, so that step reads Q directly; with c = 2 the C step
+    // reads row kc+1 from U, so it is copied there.
+    if (c == 2) TRY(copy_rows(U + BQ, c * BQ, Q, BQ, K1, BQ, st));
     s0 = 1;
   }
   for (int s = s0; s + 1 < c; ++s) {
     Fam f;
     f.ntasks = K1; f.blk0 = s; f.blk_step = c;
     f.x = U + (int64_t)s * BQ; f.x_ts = c * BQ;
+    if (s == 1 && Q) {  // row kc+1 lives in Q (contiguous rows)
+      f.x = Q; f.x_ts = BQ;
+    }
     f.s = src_fam(src, mode, BQ, s + 1); f.s_ts = c * BQ;
     f.out = U + (int64_t)(s + 1) * BQ; f.out_ts = c * BQ;
     TRY(family(S, B, E_PROP, f, st));
