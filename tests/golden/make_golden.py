@@ -148,7 +148,28 @@ def conv_relu_case():
     solve_case("conv_relu_d16_c4x8x8", net, xs, [1, 7], 4, threshold=1)
 
 
+def netfile_case():
+    """A network file written by the reference's own save_network (network.py:199-216, .json + LE
+    float64 .bin in declaration order), with the arrays it holds, for the loader parity test."""
+    net = L.random_network(8, 6, [5, 8, 6], input_dim=4, num_classes=3)
+    L.save_network(net, os.path.join(OUT, "net_dense_8x6"))
+    np.savez_compressed(os.path.join(OUT, "net_dense_8x6_arrays.npz"), **_net_arrays(net))
+    rng = np.random.default_rng([9, 2])
+    blocks = [L.conv2d_params(rng.normal(0, 0.2, (3, 3, 2, 2)), rng.normal(0, 0.05, 2), "relu", 3, 4)
+              for _ in range(3)]
+    opening = L.dense_params(rng.normal(0, 0.3, (24, 5)), rng.normal(0, 0.1, 24), "tanh")
+    readout = L.dense_params(rng.normal(0, 0.3, (3, 24)), np.zeros(3), "identity")
+    cnet = L.ResidualNetwork(opening=opening, blocks=blocks, step_size=0.25, readout=readout)
+    L.save_network(cnet, os.path.join(OUT, "net_conv_3x2x3x4"))
+    np.savez_compressed(os.path.join(OUT, "net_conv_3x2x3x4_arrays.npz"), **_net_arrays(cnet))
+    print("network files written")
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["--only", "netfile"]:
+        netfile_case()
+        sys.exit(0)
+    netfile_case()
     kat()
     net, xs, labs = experiment(64, 32, nsamp=3)
     solve_case("c1_64x32_cf4", net, xs, labs, 4)
