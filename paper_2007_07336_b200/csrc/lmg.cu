@@ -418,7 +418,28 @@ int launch_cfg(const StepArgs& a, cudaStream_t st) {
   // algorithmic work: 2MNK per task + ~5 epilogue flops per output (2q^2+5q per F)
   const double flops = (double)a.ntasks * ((double)a.M * a.N * (2.0 * a.K + 5.0));
   const double bytes = 8.0 * a.ntasks * ((double)a.N * a.K + (double)a.M * a.K + 2.0 * a.M * a.N);
-  return launch(cls, flops, bytes, st, [&] { kern<<<grid, C::NTHREADS, C::SMEM, st>>>(a); });
+  // programmatic dependent launch only for single-wave grids (the small-batch steps): with more
+  // waves, dependents launched at the last wave's start park in griddepcontrol.wait on SM slots
+  // the primary still needs (c2 measured 1.58 s vs 1.08 s per step with PDL on every launch)
+  static const bool pdl_on = getenv("LMG_NO_PDL") == nullptr;
+  static const int per_sm = [] {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, step_gemm<T, AK, BKM, ASC, VEC, FULL>,
+                                                  C::NTHREADS, C::SMEM);
+    return n;
+  }();
+  const bool pdl = pdl_on && (int64_t)grid.x * grid.y * grid.z <= (int64_t)per_sm * 148;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = dim3(C::NTHREADS, 1, 1);
+  lc.dynamicSmemBytes = C::SMEM;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl ? 1 : 0;
+  return launch(cls, flops, bytes, st, [&] { cudaLaunchKernelEx(&lc, kern, a); });
 }
 
 // residual partial slots are per TSmall n-tile

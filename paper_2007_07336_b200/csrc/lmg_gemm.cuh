@@ -357,10 +357,44 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     lb.load(base + C::A_SZ * (ASC ? 2 : 1), kt, k0, a.K, kfull);
   };
 
+  // Programmatic dependent launch: when B is the weight stack (forward / adjoint layouts) its
+  // first stages do not depend on the previous launch, so they are fetched before waiting for it
+  // (griddepcontrol.wait is a no-op without PDL); everything produced upstream -- A, the scales,
+  // every epilogue operand -- is read only after the wait, and every write happens after it, so
+  // there is no WAR hazard either.  The trigger lets the NEXT step's prologue overlap this one's
+  // tail; the parameter-gradient launch (it writes W) never triggers.
+  if (AK) {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s >= KT) break;
+      double* base = smem + s * C::STAGE + C::A_SZ * (ASC ? 2 : 1);
+      if (FULL) {
+        lb.load_next(base);
+      } else {
+        const int k0 = s * BK;
+        lb.load(base, s, k0, a.K, kfull_all || (k0 + BK <= a.K));
+      }
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (a.epi != E_PGRAD) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(s, s);
-    cp_commit();
+    if (s < KT) {
+      double* base = smem + s * C::STAGE;
+      if (FULL) {
+        la.load_next(base);
+        if (ASC) ld_.load_next(base + C::A_SZ);
+        if (!AK) lb.load_next(base + C::A_SZ * (ASC ? 2 : 1));
+      } else {
+        const int k0 = s * BK;
+        const bool kfull = kfull_all || (k0 + BK <= a.K);
+        la.load(base, s, k0, a.K, kfull);
+        if (ASC) ld_.load(base + C::A_SZ, s, k0, a.K, kfull);
+        if (!AK) lb.load(base + C::A_SZ * (ASC ? 2 : 1), s, k0, a.K, kfull);
+      }
+    }
+    cp_commit();  // group 0 also carries the prefetched weight stages
   }
 
   const int wm0 = wm * C::WTM, wn0 = wn * C::WTN;
