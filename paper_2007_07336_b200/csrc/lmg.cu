@@ -747,6 +747,25 @@ inline const double* src_fam(const double* src, int mode, int64_t BQ, int j0) {
 
 unsigned long long* g_sweep_trace = nullptr;  // lmg_debug_sweep_trace
 
+// Instantiated cycle graphs, reused across solves: a training step reissues the same solves on
+// the same buffers every step, and capturing + instantiating ~100 launches per solve cost
+// milliseconds of host time (visible at small batches).  The key holds every parameter the
+// captured launches depend on.
+struct CycleKey {
+  lmg_system fine;
+  int nlevels, c, B, src_mode;
+  const void *states, *src, *work, *trace;
+};
+struct CycleGraph {
+  CycleKey key;
+  cudaGraphExec_t exec;
+  unsigned long long launches, used;
+};
+std::mutex g_graph_mu;
+std::vector<CycleGraph> g_graphs;
+unsigned long long g_graph_clock = 0;
+constexpr size_t kGraphCacheSize = 16;
+
 bool sweep_disabled() {
   static const bool v = getenv("LMG_NO_SWEEP") != nullptr;
   return v;
@@ -1633,14 +1652,8 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
   // Cycles 2.. issue an identical launch sequence: capture it once as a CUDA graph and replay
   // it (one host call per cycle instead of ~100 launches).  Not under per-launch timing.
   const bool use_graph = !g_timing && !getenv("LMG_NO_GRAPH");
-  cudaGraphExec_t gexec = nullptr;
+  cudaGraphExec_t gexec = nullptr;  // owned by the cycle-graph cache (g_graphs)
   unsigned long long graph_launches = 0;
-  struct GraphGuard {
-    cudaGraphExec_t* g;
-    ~GraphGuard() {
-      if (*g) cudaGraphExecDestroy(*g);
-    }
-  } guard{&gexec};
   // Device-side loop (opt-in, LMG_DEVLOOP=1): cycles 2.. run inside a conditional WHILE graph
   // node whose body is one cycle + k_cycle_book; the loop leaves the device only when some sample
   // converges (to park it) or at max_cycles.  Correct (GPU tests pass with it), but measured
@@ -1742,18 +1755,44 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
     }
     if (use_graph && cyc > 0) {
       if (!gexec) {
-        cudaGraph_t graph;
-        const unsigned long long n0 = g_launches.load();
-        CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-        int rc = cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, true);
-        cudaError_t ce = cudaStreamEndCapture(st, &graph);
-        if (rc != LMG_OK) return rc;
-        if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-        graph_launches = g_launches.load() - n0;
-        ce = cudaGraphInstantiate(&gexec, graph, 0);
-        cudaGraphDestroy(graph);
-        if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
-        g_launches -= graph_launches;  // counted per replay below
+        CycleKey key;
+        std::memset(&key, 0, sizeof(key));
+        key.fine = *fine;
+        key.nlevels = nlevels; key.c = c; key.B = B; key.src_mode = src_mode;
+        key.states = states; key.src = src; key.work = work; key.trace = g_sweep_trace;
+        {
+          std::lock_guard<std::mutex> lk(g_graph_mu);
+          for (auto& e : g_graphs)
+            if (!std::memcmp(&e.key, &key, sizeof(key))) {
+              gexec = e.exec;
+              graph_launches = e.launches;
+              e.used = ++g_graph_clock;
+              break;
+            }
+        }
+        if (!gexec) {
+          cudaGraph_t graph;
+          const unsigned long long n0 = g_launches.load();
+          CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          int rc = cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, true);
+          cudaError_t ce = cudaStreamEndCapture(st, &graph);
+          if (rc != LMG_OK) return rc;
+          if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+          graph_launches = g_launches.load() - n0;
+          ce = cudaGraphInstantiate(&gexec, graph, 0);
+          cudaGraphDestroy(graph);
+          if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+          g_launches -= graph_launches;  // counted per replay below
+          std::lock_guard<std::mutex> lk(g_graph_mu);
+          if (g_graphs.size() >= kGraphCacheSize) {  // evict the least recently used entry
+            size_t lru = 0;
+            for (size_t i = 1; i < g_graphs.size(); ++i)
+              if (g_graphs[i].used < g_graphs[lru].used) lru = i;
+            cudaGraphExecDestroy(g_graphs[lru].exec);
+            g_graphs.erase(g_graphs.begin() + lru);
+          }
+          g_graphs.push_back(CycleGraph{key, gexec, graph_launches, ++g_graph_clock});
+        }
       }
       CUDA_TRY(cudaGraphLaunch(gexec, st));
       g_launches += graph_launches;

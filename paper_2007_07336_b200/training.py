@@ -153,7 +153,7 @@ class AdjointResult:
 def backward(dnet: DeviceNet, U, X, labels, *, adjoint: str = "sequential", coarsening: int = 4,
              threshold: int | None = None, tol: float = 1e-9, max_cycles: int = 50,
              scale: float = 1.0, lr: float = 0.0, want_grads: bool = True, lam_buf=None, D_buf=None,
-             block_grads: bool = True, work=None):
+             block_grads: bool = True, work=None, head_buf=None):
     """Loss + adjoint + parameter gradients for a batch at forward states U (N, B, q).
 
     Parameter gradients are summed over the batch and multiplied by ``scale`` (1/B gives the
@@ -174,6 +174,9 @@ def backward(dnet: DeviceNet, U, X, labels, *, adjoint: str = "sequential", coar
     logits = _dense_apply(dnet.Wr, dnet.br, dnet.read_act, final)
     loss, dl = softmax_ce(logits, labels)
     g_final, gWr, gbr = _dense_vjp(dnet.Wr, dnet.br, dnet.read_act, final, dl)  # training.py:213
+    if head_buf is not None:  # a stable pointer lets lmg_solve reuse its cycle graph every step
+        head_buf.copy_(g_final)
+        g_final = head_buf
     # act'(pre) at every layer's forward state
     D = D_buf if D_buf is not None else t.empty_like(U)
     _lib.call("lmg_act_deriv", view.desc(), B, U.data_ptr(), D.data_ptr(), st)
@@ -369,12 +372,23 @@ class DeviceTrainer:
                           t.empty(shape, dtype=t.float64, device=device))
         return self._bufs[1:]
 
+    def _head(self, which, B, device):
+        """Persistent (B, q) source heads (0: opened input, 1: adjoint head): stable pointers
+        let the library replay its cached cycle graphs step after step."""
+        t = require_cuda()
+        heads = self.__dict__.setdefault("_heads", {})
+        key = (which, B, str(device))
+        if key not in heads:
+            heads[key] = t.empty((B, self.dnet.width), dtype=t.float64, device=device)
+        return heads[key]
+
     def forward(self, X):
         """FAS forward solve of the batch X (B, d_in) -> states (N, B, q), report arrays."""
         dnet = self.dnet
         view = dnet._lmg_view()
         U, _, _ = self._buffers(X.shape[0], X.device)
-        f0 = _dense_apply(dnet.Wo, dnet.bo, dnet.open_act, X)
+        f0 = self._head(0, X.shape[0], X.device)
+        f0.copy_(_dense_apply(dnet.Wo, dnet.bo, dnet.open_act, X))
         hist, cyc, conv = solve_device(view, self.nlevels, self.c, f0, U, src_mode=_lib.SRC_HEAD,
                                        use_initial=False, tol=self.tol, max_cycles=self.max_cycles)
         return U, hist, cyc, conv
@@ -386,7 +400,8 @@ class DeviceTrainer:
         _, lam, D = self._buffers(X.shape[0], X.device)
         r = backward(self.dnet, U, X, labels, adjoint=self.adjoint, coarsening=self.c,
                      threshold=self.threshold, tol=self.adj_tol, max_cycles=self.adj_max_cycles,
-                     scale=1.0 / X.shape[0], lr=self.lr, want_grads=False, lam_buf=lam, D_buf=D)
+                     scale=1.0 / X.shape[0], lr=self.lr, want_grads=False, lam_buf=lam, D_buf=D,
+                     head_buf=self._head(1, X.shape[0], X.device))
         return StepResult(r.loss, hist, cyc, conv, r.hist, r.cycles, r.converged)
 
     # -- batch slices on concurrent streams ------------------------------------------------------
