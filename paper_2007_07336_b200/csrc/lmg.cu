@@ -760,6 +760,7 @@ struct CycleGraph {
   CycleKey key;
   cudaGraphExec_t exec;
   unsigned long long launches, used;
+  int in_use;  // solves currently replaying it (concurrent batch slices): never evicted then
 };
 std::mutex g_graph_mu;
 std::vector<CycleGraph> g_graphs;
@@ -1654,6 +1655,15 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
   const bool use_graph = !g_timing && !getenv("LMG_NO_GRAPH");
   cudaGraphExec_t gexec = nullptr;  // owned by the cycle-graph cache (g_graphs)
   unsigned long long graph_launches = 0;
+  struct InUse {  // releases this solve's hold on its cached graph
+    cudaGraphExec_t* g;
+    ~InUse() {
+      if (!*g) return;
+      std::lock_guard<std::mutex> lk(g_graph_mu);
+      for (auto& e : g_graphs)
+        if (e.exec == *g) --e.in_use;
+    }
+  } in_use_guard{&gexec};
   // Device-side loop (opt-in, LMG_DEVLOOP=1): cycles 2.. run inside a conditional WHILE graph
   // node whose body is one cycle + k_cycle_book; the loop leaves the device only when some sample
   // converges (to park it) or at max_cycles.  Correct (GPU tests pass with it), but measured
@@ -1767,6 +1777,7 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
               gexec = e.exec;
               graph_launches = e.launches;
               e.used = ++g_graph_clock;
+              ++e.in_use;
               break;
             }
         }
@@ -1784,14 +1795,17 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
           if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
           g_launches -= graph_launches;  // counted per replay below
           std::lock_guard<std::mutex> lk(g_graph_mu);
-          if (g_graphs.size() >= kGraphCacheSize) {  // evict the least recently used entry
-            size_t lru = 0;
-            for (size_t i = 1; i < g_graphs.size(); ++i)
-              if (g_graphs[i].used < g_graphs[lru].used) lru = i;
-            cudaGraphExecDestroy(g_graphs[lru].exec);
-            g_graphs.erase(g_graphs.begin() + lru);
+          if (g_graphs.size() >= kGraphCacheSize) {  // evict the least recently used idle entry
+            size_t lru = g_graphs.size();
+            for (size_t i = 0; i < g_graphs.size(); ++i)
+              if (g_graphs[i].in_use == 0 && (lru == g_graphs.size() || g_graphs[i].used < g_graphs[lru].used))
+                lru = i;
+            if (lru < g_graphs.size()) {
+              cudaGraphExecDestroy(g_graphs[lru].exec);
+              g_graphs.erase(g_graphs.begin() + lru);
+            }
           }
-          g_graphs.push_back(CycleGraph{key, gexec, graph_launches, ++g_graph_clock});
+          g_graphs.push_back(CycleGraph{key, gexec, graph_launches, ++g_graph_clock, 1});
         }
       }
       CUDA_TRY(cudaGraphLaunch(gexec, st));
