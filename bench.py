@@ -355,6 +355,11 @@ def run_ours(args, cfg):
             dist.barrier()
         torch.cuda.synchronize()
 
+    import gc
+
+    # no Python GC pauses inside the timed regions (short, sync-heavy steps like c5 saw them)
+    gc.collect()
+    gc.disable()
     res = None
     for _ in range(args.warmup):
         res = tr.step(X, labels)
@@ -513,6 +518,7 @@ def run_ours(args, cfg):
                      f"; model-partitioned over {world} ranks (each rank propagates its layers "
                      "and hands the state to the next, LayerParallelTrainer.serial_step)")),
             fas_over_serial_time=ms / serial_ms)
+    gc.enable()
     line["clocks"] = clk.summary()
     if rank == 0:
         print(json.dumps(line))
