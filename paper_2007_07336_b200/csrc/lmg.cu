@@ -428,7 +428,13 @@ int launch_cfg(const StepArgs& a, cudaStream_t st) {
                                                   C::NTHREADS, C::SMEM);
     return n;
   }();
-  const bool pdl = pdl_on && (int64_t)grid.x * grid.y * grid.z <= (int64_t)per_sm * 148;
+  // multi-wave grids: opt-in (LMG_PDL_MULTI=1), with the trigger after the mainloop -- measured
+  // within noise on c2 (1068 vs 1066-1125 ms per step)
+  static const bool pdl_multi = getenv("LMG_PDL_MULTI") != nullptr;
+  const bool single = (int64_t)grid.x * grid.y * grid.z <= (int64_t)per_sm * 148;
+  const bool pdl = pdl_on && (single || pdl_multi);
+  StepArgs al = a;  // the launched copy carries the trigger placement
+  al.pdl_late = single ? 0 : 1;
   cudaLaunchConfig_t lc = {};
   lc.gridDim = grid;
   lc.blockDim = dim3(C::NTHREADS, 1, 1);
@@ -439,7 +445,7 @@ int launch_cfg(const StepArgs& a, cudaStream_t st) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = pdl ? 1 : 0;
-  return launch(cls, flops, bytes, st, [&] { cudaLaunchKernelEx(&lc, kern, a); });
+  return launch(cls, flops, bytes, st, [&] { cudaLaunchKernelEx(&lc, kern, al); });
 }
 
 // residual partial slots are per TSmall n-tile

@@ -61,6 +61,7 @@ struct StepArgs {
   double* part; int64_t part_slot0; int part_ld;
   int accum;  // E_PGRAD: add the gradient already in out2 (accumulate over batch slices)
   double h2;  // E_PROP with out2: out2 = x + h2*act(pre) (the coarse step's advance, same pre)
+  int pdl_late;  // programmatic launch trigger after the mainloop (multi-wave grids), not at start
 };
 
 __device__ __forceinline__ double act_fwd(int a, double v) {
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     }
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (a.epi != E_PGRAD) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (a.epi != E_PGRAD && !a.pdl_late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < KT) {
@@ -438,6 +439,9 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     }
   }
   cp_wait<0>();
+  // multi-wave grids trigger here: the dependent grid launches once every CTA has reached its
+  // epilogue, i.e. while the last wave finishes, instead of parking on slots the grid still needs
+  if (a.epi != E_PGRAD && a.pdl_late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // ---------------------------------------------------------------- fused epilogue
   EpiPtrs q;
