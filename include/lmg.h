@@ -79,6 +79,26 @@ unsigned long long lmg_launch_count(void);
 int lmg_timing_enable(int on);
 int lmg_timing_read(int cls, double* ms_total, double* flops_total, double* bytes_total,
                     unsigned long long* launches);
+/* Instrumentation: launches per kernel variant since load, written to out[0..n) in this order;
+ * returns the number of variants (LMG_ROUTE_N).  Lets tests assert which kernels a call ran. */
+enum {
+  LMG_ROUTE_STEP_SMALL = 0,      /* step_gemm 32x32 tile, predicated loads            */
+  LMG_ROUTE_STEP_SMALL_FULL = 1, /* step_gemm 32x32 tile, fully tiled shape            */
+  LMG_ROUTE_STEP_WIDE = 2,       /* step_gemm 32x64                                    */
+  LMG_ROUTE_STEP_WIDE_FULL = 3,
+  LMG_ROUTE_STEP_TINY = 4,       /* step_gemm 16x32 (batches <= 16)                    */
+  LMG_ROUTE_STEP_TINY_FULL = 5,
+  LMG_ROUTE_TGEMM_BIG = 6,       /* warp-specialised TMA step GEMM, 64x64 tiles        */
+  LMG_ROUTE_TGEMM_SMALL = 7,     /* same, 16x32 tiles                                  */
+  LMG_ROUTE_SERIAL_SPLITK = 8,   /* split-K cluster kernel for serial single-task steps */
+  LMG_ROUTE_SWEEP_FCF = 9,       /* fused persistent FCF sweep of a level               */
+  LMG_ROUTE_SWEEP_SEQ = 10,      /* fused persistent serial solve                       */
+  LMG_ROUTE_CONV_FWD = 11,       /* implicit-GEMM conv2d, forward step                  */
+  LMG_ROUTE_CONV_ADJ = 12,       /* conv2d adjoint step                                 */
+  LMG_ROUTE_CONV_PGRAD = 13,     /* conv2d parameter gradients                          */
+  LMG_ROUTE_N = 14
+};
+int lmg_route_counts(unsigned long long* out, int n);
 /* Debug: device buffer (>= 4 u64 per step, or NULL to stop) receiving per-step %globaltimer
  * stamps (step start, state ready, mainloop done, epilogue done) of chain 0 / CTA 0 of every
  * fused persistent sweep launch.  Classes 4/5 of lmg_timing_read are those launches. */

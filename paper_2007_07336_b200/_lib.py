@@ -56,6 +56,7 @@ SIGNATURES = {
     "lmg_last_error": (ctypes.c_char_p, []),
     "lmg_launch_count": (ctypes.c_ulonglong, []),
     "lmg_timing_enable": (_I, [_I]),
+    "lmg_route_counts": (_I, [ctypes.POINTER(ctypes.c_ulonglong), _I]),
     "lmg_debug_sweep_trace": (_I, [_P]),
     "lmg_debug_sweep_clusters": (_I, [_I, _I, _I]),
     "lmg_timing_read": (_I, [_I, c_double_p, c_double_p, c_double_p,
@@ -148,6 +149,20 @@ def stream_handle(device=None) -> int:
 
 def launch_count() -> int:
     return int(load().lmg_launch_count())
+
+
+ROUTES = ("step_small", "step_small_full", "step_wide", "step_wide_full", "step_tiny",
+          "step_tiny_full", "tgemm_big", "tgemm_small", "serial_splitk", "sweep_fcf", "sweep_seq",
+          "conv_fwd", "conv_adj", "conv_pgrad")
+
+
+def route_counts() -> dict:
+    """Launches per kernel variant since the library was loaded (include/lmg.h LMG_ROUTE_*)."""
+    buf = (ctypes.c_ulonglong * len(ROUTES))()
+    n = load().lmg_route_counts(buf, len(ROUTES))
+    if n != len(ROUTES):
+        raise RuntimeError(f"liblmg reports {n} route counters, expected {len(ROUTES)}")
+    return dict(zip(ROUTES, (int(v) for v in buf)))
 
 
 def timing_enable(on: bool) -> None:

@@ -344,6 +344,10 @@ struct Rec {
 };
 
 std::atomic<unsigned long long> g_launches{0};
+// per-kernel-variant launch counters (lmg_route_counts): which kernel each step actually ran on,
+// so the parity tests can assert they exercised the routing the bench times
+std::atomic<unsigned long long> g_route[LMG_ROUTE_N];
+inline void route(int r) { g_route[r].fetch_add(1, std::memory_order_relaxed); }
 bool g_timing = false;
 std::vector<Rec> g_recs;
 std::mutex g_rec_mu;  // several host threads (one per stream) may launch concurrently
@@ -433,6 +437,9 @@ int launch_cfg(const StepArgs& a, cudaStream_t st) {
   static const bool pdl_multi = getenv("LMG_PDL_MULTI") != nullptr;
   const bool single = (int64_t)grid.x * grid.y * grid.z <= (int64_t)per_sm * 148;
   const bool pdl = pdl_on && (single || pdl_multi);
+  route(std::is_same<T, TTiny>::value ? (FULL ? LMG_ROUTE_STEP_TINY_FULL : LMG_ROUTE_STEP_TINY)
+        : std::is_same<T, TWide>::value ? (FULL ? LMG_ROUTE_STEP_WIDE_FULL : LMG_ROUTE_STEP_WIDE)
+                                        : (FULL ? LMG_ROUTE_STEP_SMALL_FULL : LMG_ROUTE_STEP_SMALL));
   StepArgs al = a;  // the launched copy carries the trigger placement
   al.pdl_late = single ? 0 : 1;
   cudaLaunchConfig_t lc = {};
@@ -535,6 +542,7 @@ int launch_serial_cfg(const StepArgs& a, int KS, cudaStream_t st) {
   const int cls = AK ? (BKM ? CLS_GEMM_FWD : CLS_GEMM_ADJ) : CLS_GEMM_PG;
   const double flops = (double)a.M * a.N * (2.0 * a.K + 5.0);
   const double bytes = 8.0 * ((double)a.N * a.K + (double)a.M * a.K + 2.0 * a.M * a.N);
+  route(LMG_ROUTE_SERIAL_SPLITK);
   return launch(cls, flops, bytes, st, [&] { cudaLaunchKernelEx(&cfg, kern, a); });
 }
 
@@ -574,6 +582,7 @@ int launch_step(Layout L, const StepArgs& a, cudaStream_t st) {
     const double flops = (double)a.ntasks * ((double)a.M * a.N * (2.0 * a.K + 5.0));
     const double bytes = 8.0 * a.ntasks * ((double)a.N * a.K + (double)a.M * a.K + 2.0 * a.M * a.N);
     cudaError_t e = cudaSuccess;
+    route(tgemm_small(plan) ? LMG_ROUTE_TGEMM_SMALL : LMG_ROUTE_TGEMM_BIG);
     TRY(launch(cls, flops, bytes, st, [&] { e = tgemm_launch(plan, L == L_ADJ, st); }));
     if (e != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("tgemm: ") + cudaGetErrorString(e));
     return LMG_OK;
@@ -628,6 +637,7 @@ int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
   // algorithmic: 2 * 9 C^2 per pixel per sample (zero padding counted as work, kernels.py:135)
   const double flops = (double)a.ntasks * 2.0 * 9.0 * g.C * g.C * (double)g.HW *
                        (V == CV_PGRAD ? (double)(a.K / g.HWp) : (double)(a.M / g.HWp));
+  route(V == CV_FWD ? LMG_ROUTE_CONV_FWD : V == CV_ADJ ? LMG_ROUTE_CONV_ADJ : LMG_ROUTE_CONV_PGRAD);
   return launch(cls, flops, 0.0, st, [&] { kern<<<grid, T::NT, SMEM, st>>>(a, g); });
 }
 
@@ -833,6 +843,7 @@ int run_sweep(const SweepArgs& a, const SweepShape& sh, double steps, double wri
   if (a.src && !a.src_head) bytes += steps * row;
   if (a.adj) bytes += steps * row;
   cudaError_t e = cudaSuccess;
+  route(a.mode == SW_SEQ ? LMG_ROUTE_SWEEP_SEQ : LMG_ROUTE_SWEEP_FCF);
   TRY(launch(a.adj ? CLS_SWEEP_ADJ : CLS_SWEEP_FWD, flops, bytes, st, [&] { e = sweep_launch(a, sh, st); }));
   if (e != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("sweep launch: ") + cudaGetErrorString(e));
   return LMG_OK;
@@ -1423,6 +1434,12 @@ extern "C" {
 int lmg_abi_version(void) { return 1; }
 
 unsigned long long lmg_launch_count(void) { return g_launches.load(); }
+
+int lmg_route_counts(unsigned long long* out, int n) {
+  if (!out || n < 0) return fail(LMG_ERR_CONFIGURATION, "route counts: bad buffer");
+  for (int i = 0; i < n && i < LMG_ROUTE_N; ++i) out[i] = g_route[i].load();
+  return LMG_ROUTE_N;
+}
 
 int lmg_timing_enable(int on) {
   std::lock_guard<std::mutex> lk(g_rec_mu);

@@ -313,6 +313,8 @@ bool tgemm_prepare(const StepArgs& a, bool adj, TgPlan** plan) {
   return true;
 }
 
+bool tgemm_small(const TgPlan* plan) { return plan->kind == 2; }
+
 cudaError_t tgemm_launch(TgPlan* plan, bool adj, cudaStream_t st) {
   TgParams& prm = plan->prm;
   cudaError_t e;

@@ -13,5 +13,7 @@ struct TgPlan;
 bool tgemm_prepare(const StepArgs& a, bool adj, TgPlan** plan);
 // launches a prepared plan and frees it
 cudaError_t tgemm_launch(TgPlan* plan, bool adj, cudaStream_t st);
+// true for the 16 x 32 small-batch tile (LMG_TGEMM=small), false for the 64 x 64 one
+bool tgemm_small(const TgPlan* plan);
 
 }  // namespace lmg
