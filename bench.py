@@ -76,105 +76,138 @@ def parse():
 # CPU side (the oracle port; the reference itself is Python and not on the GPU box)
 
 
-def _blas_threads():
-    try:
-        from threadpoolctl import threadpool_info
-
-        n = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"]
-        return max(n) if n else 1
-    except Exception:  # pragma: no cover
-        return os.cpu_count() or 1
+_POOL = {}  # the parent's network + config, inherited by the forked workers (copy-on-write)
 
 
-_NET_CACHE = {}
-
-
-def cpu_reference_sample(cfg, fwd_cycles: int, nsamp: int | None = None):
-    """Time the oracle (numpy restatement of the reference path, all host BLAS threads) on a
-    bounded sample of the workload: `nsamp` samples, initial residual + 2 forward FAS cycles +
-    the reference's sequential adjoint; the forward is extrapolated linearly to `fwd_cycles`
-    cycles (every cycle does the same work).  Returns (layer*samples/s, dict)."""
-    import numpy as np
-
+def _cpu_net(cfg):
+    """The oracle network of a config (host arrays), built once per process."""
     from oracle import fas
 
     N, q = cfg["depth"], cfg["width"]
-    nsamp = nsamp or min(cfg["batch"], max(4, min(8, os.cpu_count() or 4)))
-    key = (N, q)
-    conv = cfg.get("kind") == "conv"
-    if key not in _NET_CACHE:
-        _NET_CACHE.clear()
-        if conv:
-            from paper_2007_07336_b200.synthetic import conv_network_arrays
+    if cfg.get("kind") == "conv":
+        from paper_2007_07336_b200.synthetic import conv_network_arrays
 
-            a = conv_network_arrays(N, cfg["channels"], cfg["side"], [0, N, cfg["channels"]],
-                                    input_dim=cfg["input_dim"])
-            fine = fas.ConvLevel(a["Wc"], a["b"], a["activation"], a["step"], a["side"], a["side"])
-            _NET_CACHE[key] = fas.Net(a["Wo"], a["bo"], "tanh", fine, a["Wr"], a["br"], "identity")
-        else:
-            _NET_CACHE[key] = fas.net_from_arrays(fas.random_network_arrays(N, q, [0, N, q]))
-    net = _NET_CACHE[key]
+        a = conv_network_arrays(N, cfg["channels"], cfg["side"], [0, N, cfg["channels"]],
+                                input_dim=cfg["input_dim"])
+        fine = fas.ConvLevel(a["Wc"], a["b"], a["activation"], a["step"], a["side"], a["side"])
+        return fas.Net(a["Wo"], a["bo"], "tanh", fine, a["Wr"], a["br"], "identity")
+    return fas.net_from_arrays(fas.random_network_arrays(N, q, [0, N, q]))
+
+
+def _cpu_one_sample(job):
+    """One sample of the training step on one host core (one process per
+    core, OPENBLAS 1 thread): FAS forward solve to tol, FAS adjoint to tol (the algorithm the GPU
+    arm runs), block gradients.  Runs to convergence -- no cycle extrapolation."""
+    b, max_cycles = job
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    from oracle import fas
+
+    cfg, net = _POOL["cfg"], _POOL["net"]
+    N, q, c, thr, tol = cfg["depth"], cfg["width"], cfg["cf"], cfg["threshold"], cfg["tol"]
     din = cfg.get("input_dim", q)
-    if conv:
-        nsamp = 1  # one conv sample already is ~20 s of host work
-    X = np.stack([fas.random_sample(din, [0, N, q, b]) for b in range(nsamp)])
-    labels = np.arange(nsamp) % 10
-    t0 = time.perf_counter()
-    src = net.source(X)
-    levels = fas.build_levels(net.blocks, cfg["cf"], cfg["threshold"])
-    U = fas.initial_guess(levels[0], src)
-    fas.l2_norms(fas.compute_residual(levels[0], U, src))
-    t1 = time.perf_counter()
-    ncyc = 1 if conv else 2
-    for _ in range(ncyc):
-        fas.mg_cycle(levels, cfg["cf"], U, src)
-    t2 = time.perf_counter()
-    final, logits = fas.adjoint_head(net, U)
-    _, dl = fas.loss_and_dlogits(logits, labels)
-    gfin, _ = fas.g_final_from(net, final, dl)
-    D = fas.derivs(net.blocks, U)
-    mu, lam0 = fas.adjoint_sequential(fas.adjoint_level(net.blocks, D), gfin)
-    fas.block_grads(net.blocks, U, mu, D, 1.0 / nsamp)
-    t3 = time.perf_counter()
-    est = (t1 - t0) + fwd_cycles * (t2 - t1) / ncyc + (t3 - t2)
-    info = dict(sample=(f"{nsamp} samples of the same workload: initial residual + {ncyc} timed "
-                        f"forward FAS cycles extrapolated to {fwd_cycles} cycles + the reference's "
-                        f"sequential adjoint and block gradients; oracle/fas.py batched numpy"),
-                cores=_blas_threads(), measured_s=t3 - t0, estimated_s=est)
-    return N * nsamp / est, info
+    with threadpool_limits(limits=1, user_api="blas"):
+        t0 = time.perf_counter()
+        X = fas.random_sample(din, [0, N, q, b])[None]
+        src = net.source(X)
+        U, fh, fconv = fas.solve(fas.build_levels(net.blocks, c, thr), c, src, tol, max_cycles)
+        final, logits = fas.adjoint_head(net, U)
+        _, dl = fas.loss_and_dlogits(logits, np.array([b % 10]))
+        gfin, _ = fas.g_final_from(net, final, dl)
+        D = fas.derivs(net.blocks, U)
+        s = np.zeros_like(U)
+        s[0] = gfin
+        adj = fas.adjoint_level(net.blocks, D)
+        mu, ah, aconv = fas.solve(fas.build_levels(adj, c, thr), c, s, tol, max_cycles)
+        fas.block_grads(net.blocks, U, mu, D, 1.0)
+        return dict(fwd=len(fh[0]) - 1, adj=len(ah[0]) - 1, converged=bool(fconv[0] and aconv[0]),
+                    final=fh[0][-1], s=time.perf_counter() - t0)
 
 
-def _all_host_threads():
-    """torchrun exports OMP_NUM_THREADS=1; the CPU arms must use every host core."""
+class CpuArm:
+    """The reference algorithm on the host cores: a pool of P forked worker processes (P = host
+    cores), one sample each per step, every sample solved to tol forward and adjoint.  A step's
+    layer*samples/s = N * P / wall seconds of the step (samples are independent; extrapolation
+    is across samples only)."""
+
+    def __init__(self, cfg, procs=None):
+        import multiprocessing as mp
+
+        self.cfg = cfg
+        self.P = procs or os.cpu_count() or 1
+        _POOL["cfg"], _POOL["net"] = cfg, _cpu_net(cfg)
+        self.pool = mp.get_context("fork").Pool(self.P)
+        self.next = 0
+
+    def step(self, max_cycles=None):
+        jobs = [((self.next + i) % self.cfg["batch"], max_cycles or self.cfg["max_cycles"])
+                for i in range(self.P)]
+        self.next += self.P
+        t0 = time.perf_counter()
+        out = self.pool.map(_cpu_one_sample, jobs, chunksize=1)
+        wall = time.perf_counter() - t0
+        return self.cfg["depth"] * len(jobs) / wall, wall, out
+
+    def warm(self):
+        """Untimed warm-up: every worker runs one bounded solve (1 cycle forward and adjoint)."""
+        return self.step(max_cycles=1)
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+    def describe(self, out, steps):
+        fwd = sorted({o["fwd"] for o in out})
+        adj = sorted({o["adj"] for o in out})
+        return (f"{self.P} forked processes x 1 BLAS thread (OPENBLAS via threadpoolctl), one "
+                f"sample each per step, {steps} step(s): FAS forward to tol {self.cfg['tol']:g} "
+                f"({'/'.join(map(str, fwd))} cycles) + FAS adjoint to tol ({'/'.join(map(str, adj))} "
+                f"cycles) + block gradients, every sample solved to convergence "
+                f"(all converged: {all(o['converged'] for o in out)}); oracle/fas.py (numpy port "
+                f"of the reference path, per-sample W @ u like the reference)")
+
+
+def cpu_reference_sample(cfg, steps=1):
+    """Bounded CPU baseline for the GPU arm's JSON line: one warm-up map + `steps` timed steps."""
+    arm = CpuArm(cfg)
     try:
-        from threadpoolctl import threadpool_limits
-
-        return threadpool_limits(limits=os.cpu_count() or 1, user_api="blas")
-    except Exception:  # pragma: no cover
-        return None
+        arm.warm()
+        vals, out = [], []
+        for _ in range(steps):
+            v, _, o = arm.step()
+            vals.append(v)
+            out += o
+        return statistics.mean(vals), dict(cores=arm.P, sample=arm.describe(out, steps))
+    finally:
+        arm.close()
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    _limits = _all_host_threads()  # noqa: F841
-    times, vals = [], []
-    info = None
-    # the number of forward cycles the solve needs at this config (c2: 36, BASELINE.md 3.1)
-    cyc = {"c2": 36, "c1": 7, "c5": 8, "c3": 16, "c4": 6}[args.config]  # measured on B200
-    for i in range(args.warmup + args.steps):
-        v, info = cpu_reference_sample(cfg, cyc)
-        if i >= args.warmup:
+    arm = CpuArm(cfg)
+    try:
+        for _ in range(args.warmup):  # bounded: one FAS cycle forward + adjoint per worker
+            arm.warm()
+        vals, times, out = [], [], []
+        for _ in range(args.steps):
+            v, wall, o = arm.step()
             vals.append(v)
-            times.append(info["estimated_s"])
-    value = statistics.mean(vals)
+            times.append(wall)
+            out += o
+    finally:
+        arm.close()
+    value = args.steps * cfg["depth"] * arm.P / sum(times)
     line = dict(metric=METRIC, value=value, unit=UNIT, n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=1e3 * statistics.mean(times), higher_is_better=True,
                 scaling="strong", vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload=cfg["workload"]), impl="reference",
-                cpu_baseline=dict(value=value, unit=UNIT, cores=info["cores"], kind="port",
-                                  sample=info["sample"]),
+                config=dict(workload=cfg["workload"], samples_per_step=arm.P,
+                            cycles_per_sample=[[o["fwd"], o["adj"]] for o in out]),
+                impl="reference",
+                cpu_baseline=dict(value=value, unit=UNIT, cores=arm.P, kind="port",
+                                  sample=arm.describe(out, args.steps)),
                 e2e=dict(value=value, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line))
 
@@ -295,6 +328,34 @@ def load_traffic(config):
         return None, None
 
 
+class ThetaSnapshot:
+    """The trainer's parameters, saved once before the warm-up and restored before every timed
+    pass (clean, instrumented, serial, e2e): each pass times the same K SGD steps from the same
+    theta, so the passes measure the same work.  The copy is outside every timed region."""
+
+    def __init__(self, torch, dnet):
+        self.live = [dnet.stack.W, dnet.stack.b, dnet.Wo, dnet.bo, dnet.Wr, dnet.br]
+        need = sum(x.numel() * x.element_size() for x in self.live)
+        where = "cuda" if need < torch.cuda.mem_get_info()[0] // 3 else "cpu"
+        self.saved = [x.detach().to(where, copy=True) for x in self.live]
+        self.torch = torch
+
+    def restore(self):
+        for d, s in zip(self.live, self.saved):
+            d.copy_(s)
+        self.torch.cuda.synchronize()
+
+
+def hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json (driver-measured on this pool), else the profiling
+    recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback 6.65 TB/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)"
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -349,6 +410,7 @@ def run_ours(args, cfg):
                              max_cycles=cfg["max_cycles"], adjoint=args.adjoint,
                              learning_rate=cfg["lr"], split=split)
     peak = fp64_peak_tflops(torch, dev)
+    theta = ThetaSnapshot(torch, tr.dnet)
 
     def barrier():
         if dist is not None:
@@ -361,11 +423,14 @@ def run_ours(args, cfg):
     gc.collect()
     gc.disable()
     res = None
+    theta.restore()
     for _ in range(args.warmup):
         res = tr.step(X, labels)
     barrier()
 
     # ---- timed region: inputs resident in HBM (no per-launch instrumentation inside)
+    theta.restore()
+    barrier()
     n0 = _lib.launch_count()
     with ClockSampler(local) as clk:
         barrier()
@@ -387,6 +452,7 @@ def run_ours(args, cfg):
 
     # ---- roofline pass: the same K steps again with a CUDA event pair around every launch of
     # the library (recorded on the launching stream), summed per kernel class
+    theta.restore()
     _lib.timing_enable(True)
     barrier()
     si, ei = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -396,8 +462,10 @@ def run_ours(args, cfg):
     ei.record()
     barrier()
     inst_ms = si.elapsed_time(ei) / args.steps
-    f_ms, f_flops, _, f_n = _lib.timing_read(0)
-    a_ms, a_flops, _, a_n = _lib.timing_read(1)
+    f_ms, f_flops, f_bytes, f_n = _lib.timing_read(0)
+    a_ms, a_flops, a_bytes, a_n = _lib.timing_read(1)
+    s_ms, s_flops, s_bytes, s_n = _lib.timing_read(6)  # split-K serial steps (latency-bound)
+    w_ms, w_flops, w_bytes, w_n = (sum(v) for v in zip(_lib.timing_read(4), _lib.timing_read(5)))
     all_ms, _, _, all_n = _lib.timing_read(-1)
     _lib.timing_enable(False)
 
@@ -419,6 +487,7 @@ def run_ours(args, cfg):
             backward(dn, Us, X, labels, adjoint="sequential", scale=1.0 / B, lr=cfg["lr"],
                      want_grads=False)
 
+        theta.restore()
         serial_step()
         barrier()
         s3, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -432,6 +501,7 @@ def run_ours(args, cfg):
     elif not conv:
         # model-partitioned serial propagation over the same ranks: each rank
         # propagates its layers and hands the state on; timed like the FAS step (max over ranks)
+        theta.restore()
         tr.serial_step(X, labels)
         barrier()
         s3, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -446,6 +516,7 @@ def run_ours(args, cfg):
         serial_ms = float(t.item())
 
     # ---- e2e: same step through the public API from pinned host buffers, result read back
+    theta.restore()
     barrier()
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s2.record()
@@ -464,10 +535,26 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # dominant kernel class: the relaxation / residual step launches (forward + adjoint layouts);
+    # bound by its arithmetic intensity against the FP64 ridge (DGEMM peak / HBM peak)
     gemm_ms = f_ms + a_ms
     gemm_flops = f_flops + a_flops
-    achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    gemm_bytes = f_bytes + a_bytes
+    hbm, hbm_src = hbm_peak()
+    intensity = gemm_flops / gemm_bytes if gemm_bytes else float("inf")
+    ridge = peak * 1e12 / (hbm * 1e9)
+    if conv or intensity >= ridge:
+        bound, unit_r, pk, pk_src = "tensor", "TFLOP/s", peak, (
+            "cuBLAS DGEMM 8192^3 measured in this run (FP64 is not in MEASURED_PEAKS.json)")
+        achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+        alg = "(2q^2+5q) flops per F-evaluation x B samples x tasks per launch"
+    else:
+        bound, unit_r, pk, pk_src = "hbm", "GB/s", hbm, hbm_src
+        achieved = gemm_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else 0.0
+        alg = ("8q^2 (W_j, read once per layer step for the whole batch) + 8qB per state row read "
+               "or written, per task, summed over the launches")
     traffic, prof = load_traffic(args.config)
+    theta_bytes = tr.dnet.stack.W.numel() * 8
     line = dict(
         metric=METRIC,
         value=N * B / (ms * 1e-3),
@@ -478,9 +565,9 @@ def run_ours(args, cfg):
                     threshold=cfg["threshold"], tol=cfg["tol"], adjoint=args.adjoint,
                     parallelism=(f"layer-partitioned x{world}" if world > 1 else
                                  f"single GPU, {getattr(tr, 'split', 1)} batch slice(s) on concurrent streams"),
-                    l2=(f"inputs larger than L2 (theta {N * q * q * 8 / 2**30:.2f} GiB, states "
+                    l2=(f"inputs larger than L2 (theta {theta_bytes / 2**30:.3f} GiB, states "
                         f"{N * B * q * 8 / 2**30:.2f} GiB), no flush"
-                        if N * q * q * 8 > 2 * 126e6 else
+                        if max(theta_bytes, N * B * q * 8) > 2 * 126e6 else
                         "theta smaller than L2: cycles re-read it from L2 (no flush; the FAS step "
                         "is latency-bound at this size)"),
                     cycles_per_step=cycles),
@@ -488,15 +575,28 @@ def run_ours(args, cfg):
                  h2d_bytes_per_step=int(X_host.numel() * 8 + lab_host.numel() * 8),
                  d2h_bytes_per_step=int(loss_host.numel() * 8), wall_ms_per_step=wall_ms),
         gpu_launches=int(launches),
-        roofline=dict(bound="tensor", achieved=achieved, peak=peak, unit="TFLOP/s",
-                      frac=achieved / peak if peak else None,
+        roofline=dict(bound=bound, achieved=achieved, peak=pk, unit=unit_r,
+                      frac=achieved / pk if pk else None,
                       traffic=traffic,
-                      kernel="layer-step GEMM class, FP64 DMMA m8n8k4 with fused FAS epilogues: "
-                             "lmg::step_gemm (forward steps) + lmg::tgemm_kernel (warp-specialised "
-                             "TMA, adjoint steps); conv configs: lmg::conv_gemm",
-                      peak_source="cuBLAS DGEMM 8192^3 measured in this run (FP64 is not in MEASURED_PEAKS.json)",
-                      algorithmic="(2q^2+5q) flops per F-evaluation x B samples x tasks per launch",
+                      kernel="relaxation/residual layer-step class, FP64 DMMA m8n8k4 with fused FAS "
+                             "epilogues: lmg::step_gemm (forward steps) + lmg::tgemm_kernel "
+                             "(warp-specialised TMA, adjoint steps); conv configs: lmg::conv_gemm",
+                      peak_source=pk_src,
+                      algorithmic=alg,
+                      intensity_flop_per_byte=intensity, fp64_ridge_flop_per_byte=ridge,
                       share_of_step=(gemm_ms / (inst_ms * args.steps)) if inst_ms else None,
+                      serial_steps=dict(
+                          what="split-K serial layer steps (coarsest exact solve): latency-bound "
+                               "chain, reported apart from the relaxation class",
+                          ms_per_step=s_ms / args.steps, launches_per_step=s_n / args.steps,
+                          tflops=(s_flops / (s_ms * 1e-3) / 1e12) if s_ms else None,
+                          share_of_step=(s_ms / (inst_ms * args.steps)) if inst_ms else None),
+                      fused_sweeps=dict(
+                          what="fused persistent FCF / serial sweeps (state on chip)",
+                          ms_per_step=w_ms / args.steps, launches_per_step=w_n / args.steps,
+                          gbs=(w_bytes / (w_ms * 1e-3) / 1e9) if w_ms else None),
+                      all_step_gemm_tflops=((gemm_flops + s_flops) / ((gemm_ms + s_ms) * 1e-3) / 1e12)
+                      if gemm_ms + s_ms > 0 else None,
                       launches=f_n + a_n, all_kernel_ms_per_step=all_ms / args.steps,
                       all_launches_per_step=all_n / args.steps,
                       measured="CUDA events around every step-GEMM launch, on its stream, over a "
@@ -504,8 +604,7 @@ def run_ours(args, cfg):
                                f"{inst_ms:.2f} ms vs {ms:.2f} ms clean)"),
     )
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        _limits = _all_host_threads()  # noqa: F841
-        v, info = cpu_reference_sample(cfg, cycles[-1][0])
+        v, info = cpu_reference_sample(cfg)
         line["cpu_baseline"] = dict(value=v, unit=UNIT, cores=info["cores"], kind="port",
                                     sample=info["sample"])
     if serial_ms is not None:

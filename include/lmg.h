@@ -72,8 +72,8 @@ const char* lmg_last_error(void);
 
 /* Instrumentation (not part of the reference API): number of kernels this library has launched,
  * and optional CUDA-event timing of every launch by class (0 forward step GEMM, 1 adjoint step
- * GEMM, 2 parameter-gradient GEMM, 3 elementwise/reduction, 4/5 fused forward/adjoint sweep;
- * -1 = all).  lmg_timing_enable(1)
+ * GEMM, 2 parameter-gradient GEMM, 3 elementwise/reduction, 4/5 fused forward/adjoint sweep,
+ * 6 split-K serial step (coarsest solve / serial propagation); -1 = all).  lmg_timing_enable(1)
  * clears the records; lmg_timing_read synchronises on the recorded events. */
 unsigned long long lmg_launch_count(void);
 int lmg_timing_enable(int on);

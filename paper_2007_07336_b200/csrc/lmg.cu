@@ -334,7 +334,9 @@ enum Cls {
   CLS_ELEM = 3,       // elementwise / reductions
   CLS_SWEEP_FWD = 4,  // fused persistent sweep (lmg_sweep.cu), forward
   CLS_SWEEP_ADJ = 5,  // fused persistent sweep, adjoint
-  CLS_N = 6
+  CLS_SERIAL = 6,     // split-K cluster kernel: one serial layer step (coarsest solve, serial
+                      // propagation) -- latency-bound, kept out of the relaxation classes 0/1
+  CLS_N = 7
 };
 
 struct Rec {
@@ -539,7 +541,7 @@ int launch_serial_cfg(const StepArgs& a, int KS, cudaStream_t st) {
   at[0].val.clusterDim.z = KS;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  const int cls = AK ? (BKM ? CLS_GEMM_FWD : CLS_GEMM_ADJ) : CLS_GEMM_PG;
+  const int cls = CLS_SERIAL;
   const double flops = (double)a.M * a.N * (2.0 * a.K + 5.0);
   const double bytes = 8.0 * ((double)a.N * a.K + (double)a.M * a.K + 2.0 * a.M * a.N);
   route(LMG_ROUTE_SERIAL_SPLITK);

@@ -7,9 +7,11 @@
   parameters agree with the serial training step;
 * a full-size training step is bit-for-bit repeatable (no races in the fused / TMA kernels).
 
-Tolerance 1e-8 relative: FAS stops at an unnormalised residual norm <= 1e-9, and the error it
-leaves is that residual carried through the remaining layers.  Measured on B200 (relative max
-gaps): c2 states 2e-13, adjoint 1e-10, block gradients 4e-11; c5 all ~5e-12."""
+Tolerances (relative max gaps): FAS stops at an unnormalised residual norm <= 1e-9, and the
+error it leaves is that residual carried through the remaining layers -- so these bound the
+solver's stopping error, not rounding (rounding is checked against the oracle, <= 1e-12, in
+test_gpu_benchshapes.py).  Measured on B200: c2 states 2e-13, adjoint 1e-10, block gradients
+4e-11; c5 ~5e-12.  Asserted: states <= 1e-11, adjoint and gradients <= 1e-9."""
 
 import numpy as np
 import pytest
@@ -71,7 +73,7 @@ def test_fas_converges_to_serial_propagation(name):
     e_gw = _rel(lam_f.gW, lam_s.gW)
     print(f"{name}: fwd {e_fwd:.2e} adj {e_adj:.2e} gW {e_gw:.2e} cycles {int(cyc.max())}"
           f"+{int(lam_f.cycles.max())}")
-    assert e_fwd <= 1e-8 and e_adj <= 1e-8 and e_gw <= 1e-8, (e_fwd, e_adj, e_gw)
+    assert e_fwd <= 1e-11 and e_adj <= 1e-9 and e_gw <= 1e-9, (e_fwd, e_adj, e_gw)
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
