@@ -174,3 +174,31 @@ class NumpyOps:
 
     def work_doubles(self, L, B, q):
         return 1
+
+    def gather_system(self, solver, l):
+        """The whole system's level l on every rank, gathered from the ranks' local levels in
+        system order (distributed.CudaOps.gather_system restated on oracle levels)."""
+        import torch
+
+        from . import fas
+
+        lev = solver.levels[l].desc()
+        g = lambda x: solver._allgather_ordered(torch.from_numpy(np.ascontiguousarray(x))).numpy()  # noqa: E731
+        if lev.kind == "adjoint":
+            f = lev.fwd
+            fwd = fas.DenseLevel(g(f.W), g(f.b), f.activation, f.step, f.exact)
+            return fas.AdjointLevel(fwd, g(lev.D), lev.step)
+        return fas.DenseLevel(g(lev.W), g(lev.b), lev.activation, lev.step, lev.exact)
+
+    def subcycle(self, gsys, nlev, c, B, V, SH):
+        """multigrid.py:216-226 on the gathered level: the exact solve, or ONE FAS cycle."""
+        from . import fas
+
+        v, sh = _a(V), _a(SH)
+        if nlev == 1:
+            v[...] = fas.sequential_forward(gsys, sh)
+            return
+        levels = [gsys]
+        for _ in range(nlev - 1):
+            levels.append(levels[-1].coarsen(c))
+        fas.mg_cycle(levels, c, v, sh)

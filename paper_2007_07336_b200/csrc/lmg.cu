@@ -346,6 +346,9 @@ struct Rec {
 };
 
 std::atomic<unsigned long long> g_launches{0};
+// launches issued by THIS host thread: a graph capture counts its own launches with it (several
+// host threads -- one per batch-slice stream -- may launch concurrently)
+thread_local unsigned long long t_launches = 0;
 // per-kernel-variant launch counters (lmg_route_counts): which kernel each step actually ran on,
 // so the parity tests can assert they exercised the routing the bench times
 std::atomic<unsigned long long> g_route[LMG_ROUTE_N];
@@ -383,6 +386,7 @@ int launch(int cls, double flops, double bytes, cudaStream_t st, F&& f) {
     g_recs.push_back(r);
   }
   ++g_launches;
+  ++t_launches;
   return LMG_OK;
 }
 
@@ -1635,6 +1639,23 @@ int lmg_solve(const lmg_system* fine, int nlevels, int c, int B, double* states,
   return rc;
 }
 
+// The current device's default stream-ordered pool keeps freed memory for reuse (release
+// threshold = unlimited), once per device.
+void keep_pool_memory() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.push_back(dev);
+}
+
 int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
              const double* src, int src_mode, int use_initial, double tol, int max_cycles,
              double* hist_host, int32_t* cycles_host, int32_t* converged_host, void* work,
@@ -1663,13 +1684,25 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
     cycles_host[b] = 0;
     if (nrm[b] <= tol) { done[b] = 1; ++ndone; }
   }
-  // samples that stop while others continue are parked here (multigrid.py:297 per sample)
-  std::vector<std::pair<int, double*>> parked;
+  // samples that stop while others continue are parked here (multigrid.py:297 per sample).
+  // Stream-ordered allocations from the device's default pool, which keeps freed memory
+  // (keep_pool_memory): with the default release threshold of 0 every synchronize returned the
+  // parked blocks to the OS and the next park re-mapped them -- c2 backward solves that park
+  // ~100 samples ran 0.7-3.9 s instead of 0.54 s.  The guard frees them on every exit path.
+  keep_pool_memory();
+  struct Parked {
+    std::vector<std::pair<int, double*>> v;
+    cudaStream_t st;
+    ~Parked() {
+      for (auto& pb : v) cudaFreeAsync(pb.second, st);
+    }
+  } parked_guard{{}, st};
+  auto& parked = parked_guard.v;
   auto park = [&](int b) -> int {
     double* buf = nullptr;
     CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&buf), (size_t)n * q * sizeof(double), st));
-    TRY(copy_rows(buf, q, states + (int64_t)b * q, BQ, n, q, st));
     parked.emplace_back(b, buf);
+    TRY(copy_rows(buf, q, states + (int64_t)b * q, BQ, n, q, st));
     return LMG_OK;
   };
   for (int b = 0; b < B && ndone < B; ++b)
@@ -1736,7 +1769,7 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
         cudaGraphNode_t node;
         CUDA_TRY(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
         cudaGraph_t body = cp.conditional.phGraph_out[0];
-        const unsigned long long n0 = g_launches.load();
+        const unsigned long long n0 = t_launches;
         CUDA_TRY(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
         int rc = cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, true);
         if (rc == LMG_OK)
@@ -1753,7 +1786,7 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
           cudaGraphDestroy(g);
           return fail(LMG_ERR_CUDA, std::string("loop capture: ") + cudaGetErrorString(ce));
         }
-        iter_launches = g_launches.load() - n0;
+        iter_launches = t_launches - n0;
         g_launches -= iter_launches;  // counted per executed iteration below
         ce = cudaGraphInstantiate(&dexec, g, 0);
         cudaGraphDestroy(g);
@@ -1808,13 +1841,13 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
         }
         if (!gexec) {
           cudaGraph_t graph;
-          const unsigned long long n0 = g_launches.load();
+          const unsigned long long n0 = t_launches;
           CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
           int rc = cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, true);
           cudaError_t ce = cudaStreamEndCapture(st, &graph);
           if (rc != LMG_OK) return rc;
           if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-          graph_launches = g_launches.load() - n0;
+          graph_launches = t_launches - n0;
           ce = cudaGraphInstantiate(&gexec, graph, 0);
           cudaGraphDestroy(graph);
           if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
@@ -1854,10 +1887,7 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
         if (done[b] && std::none_of(parked.begin(), parked.end(), [&](auto& pb) { return pb.first == b; }))
           TRY(park(b));
   }
-  for (auto& pb : parked) {
-    TRY(copy_rows(states + (int64_t)pb.first * q, BQ, pb.second, q, n, q, st));
-    CUDA_TRY(cudaFreeAsync(pb.second, st));
-  }
+  for (auto& pb : parked) TRY(copy_rows(states + (int64_t)pb.first * q, BQ, pb.second, q, n, q, st));
   for (int b = 0; b < B; ++b) converged_host[b] = done[b];
   CUDA_TRY(cudaStreamSynchronize(st));
   return LMG_OK;

@@ -1,19 +1,22 @@
 """Layer-parallel FAS across GPUs: the reference's worker partition (parallel.py:61-79) mapped to
 ranks, one process per GPU, halos over NCCL (NVLink) via torch.distributed.
 
-Each rank owns a contiguous run of whole blocks at every relaxed level (requires
-N_l % (world * c) == 0 for every relaxed level l -- the reference's assignment k // ceil(nb/P) is
-then an equal split) and the matching rows of the coarsest level.  Per cycle and cross edge:
+Each rank owns a contiguous run of whole blocks at the finest level (requires N % (world * c) == 0
+-- the reference's assignment k // ceil(nb/P) is then an equal split) and at every coarse level
+that still splits into whole blocks; the first level that does not (at the latest the coarsest)
+is gathered and the sub-hierarchy below it runs replicated on every rank (check_partition).  Per
+cycle and cross edge:
 
   after FCF part A : U[L]            1 row   (the reference's one BoundaryMessage per edge per
                                               C-sweep, parallel.py:183-216)
   after FCF part B : P[nb], adv_out  2 rows  (C-row residual and coarse-source halo)
-  coarsest level   : gathered (default, north_star / SURVEY 8e): S_H rows, and once per solve the
-                     coarse theta (+ act' rows for the adjoint), are all-gathered; every rank
-                     runs the same exact forward substitution of the whole coarse grid and keeps
-                     its rows (the scatter becomes local slicing).  LMG_COARSEST=pipeline: each
-                     rank solves its rows and hands its last state to the next (1 row per edge,
-                     no theta replication).
+  gathered level   : (the coarsest by default, north_star / SURVEY 8e) S_H rows (+ the injected
+                     iterate V when it is not the coarsest), and once per solve its theta
+                     (+ act' rows for the adjoint), are all-gathered; every rank runs the same
+                     exact solve / one FAS cycle of the gathered sub-hierarchy and keeps its rows
+                     (the scatter becomes local slicing).  LMG_COARSEST=pipeline (coarsest level
+                     only): each rank solves its rows and hands its last state to the next
+                     (1 row per edge, no theta replication).
   norms            : all_gather of per-block partials (B doubles per block), summed in global
                      block order -> bitwise the single-GPU norms.
 
@@ -116,6 +119,60 @@ class CudaOps:
     def work_doubles(self, L, B, q):
         return _lib.load().lmg_local_workspace(L, B, q) // 8 + 1
 
+    def gather_system(self, solver, l):
+        """Level l of the WHOLE system on every rank: the rows of each rank's local level l in
+        SYSTEM order -- forward: each rank's local layers j*s in rank order; adjoint (reversed
+        system, multigrid.py:101 applied to it): each rank's local layers L-1-j*s, ranks in
+        reverse order -- plus the adjoint's act' rows.  Gathered once per solve (theta changes
+        only between steps)."""
+        import ctypes
+
+        t = solver.t
+        lev = solver.levels[l]
+        view = lev.view
+        st = view.stack
+        n, s = lev.L, view.stride
+        adj = lev.adjoint_D is not None
+        base = st.num_blocks - 1 if adj else 0
+        idx = t.arange(n, device=st.W.device) * (-s if adj else s) + base
+
+        def gathered(x):
+            return solver._allgather_ordered(x)
+
+        Wg = gathered(st.W.index_select(0, idx))
+        bg = None if adj else gathered(st.b.index_select(0, idx))
+        Dg = gathered(lev.adjoint_D.index_select(0, idx)) if adj else None
+        loc = lev.desc()
+        d = _lib.LmgSystem()
+        ctypes.memmove(ctypes.byref(d), ctypes.byref(loc), ctypes.sizeof(d))  # kind, act, step, geometry
+        d.num_layers = n * solver.world
+        d.W, d.w_stride = Wg.data_ptr(), Wg[0].numel()
+        if adj:
+            d.b, d.b_stride = None, 0
+            d.D, d.d_stride = Dg.data_ptr(), Dg[0].numel()
+        else:
+            d.b, d.b_stride = bg.data_ptr(), bg[0].numel()
+        return (Wg, bg, Dg, d)  # the gathered tensors stay alive with the descriptor
+
+    def subcycle(self, gsys, nlev, c, B, V, SH):
+        """The gathered sub-hierarchy at its top level: the exact solve (one level) or ONE FAS
+        cycle without the residual norm -- exactly the single-GPU recursive call
+        (multigrid.py:216-226), so the result is bitwise the one-GPU solve."""
+        d = gsys[3]
+        if nlev == 1:
+            _lib.call("lmg_sequential_forward", d, B, SH.data_ptr(), _lib.SRC_DENSE, V.data_ptr(),
+                      self._st())
+            return
+        key = (d.num_layers, d.width, nlev, c, B)
+        wss = self.__dict__.setdefault("_sub_ws", {})
+        if key not in wss:
+            nbytes = _lib.load().lmg_solver_workspace(d, nlev, c, B)
+            wss[key] = (require_cuda().empty(nbytes, dtype=require_cuda().uint8, device=V.device),
+                        nbytes)
+        ws, nbytes = wss[key]
+        _lib.call("lmg_mg_cycle", d, nlev, c, B, V.data_ptr(), SH.data_ptr(), _lib.SRC_DENSE, None,
+                  ws.data_ptr(), nbytes, self._st())
+
 
 class LocalLevel:
     """This rank's view of one level: L local layers (nb blocks) of a system view."""
@@ -140,16 +197,27 @@ class LocalLevel:
 
 
 def check_partition(N, c, nlevels, world):
-    """Every relaxed level must split into whole blocks, equally over the ranks."""
+    """The level from which the hierarchy is gathered (replicated on every rank).
+
+    Levels above it are partitioned: each rank owns an equal contiguous run of whole blocks (the
+    reference's assignment k // ceil(nb/P), parallel.py:76-78, is then an equal split).  The
+    first coarse level that does not split into whole blocks over the ranks -- at the latest the
+    coarsest level -- collapses: its rows are gathered and the remaining sub-hierarchy (one FAS
+    cycle, or the exact solve at the coarsest level, multigrid.py:216-226) runs on every rank,
+    each keeping its own rows.  So c5 (cf 16, levels [1024, 64, 4]) at 8 ranks partitions the
+    fine level (8 blocks per rank) and gathers [64, 4].  The finest level must split."""
+    if nlevels > 1 and N % (world * c):
+        raise ConfigurationError(
+            f"layer-partitioned solve needs the finest level divisible by world*c; "
+            f"{N} layers, world {world}, c {c}")
+    if N % world:
+        raise ConfigurationError(f"{N} layers do not split over {world} ranks")
     n = N
-    for _ in range(nlevels - 1):
-        if n % (world * c):
-            raise ConfigurationError(
-                f"layer-partitioned solve needs every relaxed level divisible by world*c; "
-                f"level with {n} layers, world {world}, c {c}")
+    for l in range(nlevels - 1):
+        if l > 0 and n % (world * c):
+            return l
         n //= c
-    if n % world:
-        raise ConfigurationError(f"coarsest level of {n} layers does not split over {world} ranks")
+    return nlevels - 1
 
 
 class DistSolver:
@@ -182,14 +250,16 @@ class DistSolver:
         self.has_next = self.next is not None
         self.c, self.nlevels, self.B = c, nlevels, B
         self.N_total = N_total
-        check_partition(N_total, c, nlevels, world)
+        self.gather_level = check_partition(N_total, c, nlevels, world)
         self.ops = ops
         t = require_cuda() if ops.name == "cuda" else __import__("torch")
         self.t = t
         self.device = device
         lv = LocalLevel(view_local, c, B, adjoint_D)
+        # local levels 0..gather_level (relaxed partitioned levels + this rank's rows of the
+        # gathered level)
         self.levels = [lv]
-        for _ in range(nlevels - 1):
+        for _ in range(self.gather_level):
             self.levels.append(self.levels[-1].coarsen())
         q = lv.q
         f64 = dict(dtype=t.float64, device=device)
@@ -197,10 +267,11 @@ class DistSolver:
         self.U, self.S, self.P, self.advH = [], [], [], []
         for l, lev in enumerate(self.levels):
             L = lev.L
+            relaxed = l < self.gather_level
             self.U.append(z(L + 1, B, q) if l > 0 else None)   # level 0 states are the caller's
             self.S.append(z(L + 1, B, q) if l > 0 else None)   # coarse sources, zero row L
-            self.P.append(z(lev.nb + 2, B, q) if l < nlevels - 1 else None)  # + [P_out, adv_out]
-            self.advH.append(z(lev.nb, B, q) if l < nlevels - 1 else None)
+            self.P.append(z(lev.nb + 2, B, q) if relaxed else None)  # + [P_out, adv_out]
+            self.advH.append(z(lev.nb, B, q) if relaxed else None)
         self.Q = z(lv.nb + 1, B, q)  # finest level: propagated rows kc+1 of the last residual
         self.q_valid = False
         self.recv1 = z(1, B, q)
@@ -273,8 +344,8 @@ class DistSolver:
 
     # -- rank-pipelined exact solve of the coarsest level (network.py:111-123) ----------------
     def _coarsest(self, l, V, SH):
-        if self.coarsest_mode == "gather" and self.world > 1:
-            return self._coarsest_gather(l, V, SH)
+        if self.world > 1 and (self.coarsest_mode == "gather" or l < self.nlevels - 1):
+            return self._gathered_level(l, V, SH)
         lev = self.levels[l]
         ops = self.ops
         if self.is_first:
@@ -301,58 +372,26 @@ class DistSolver:
         dist.all_gather(parts, x.contiguous(), group=self.group)
         return t.cat(parts, 0)
 
-    def _global_coarse_system(self, l):
-        """The coarsest level of the whole system on every rank, gathered once per solve (theta
-        changes only between steps): its blocks in SYSTEM order -- forward: each rank's local
-        layers j*s in rank order; adjoint (reversed system, multigrid.py:101 applied to it): each
-        rank's local layers L-1-j*s, ranks in reverse order -- plus the adjoint's act' rows."""
-        import ctypes
-
-        if self._gsys is not None:
-            return self._gsys
-        t = self.t
-        lev = self.levels[l]
-        view = lev.view
-        st = view.stack
-        n, s = lev.L, view.stride
-        adj = lev.adjoint_D is not None
-        base = st.num_blocks - 1 if adj else 0
-        idx = t.arange(n, device=st.W.device) * (-s if adj else s) + base
+    def _allgather_ordered(self, x):
+        """all_gather of this rank's rows, concatenated in SYSTEM order (rank order forward,
+        reversed rank order for the adjoint system)."""
+        parts = self._allgather(x).view(self.world, *x.shape)
         order = range(self.world - 1, -1, -1) if self.reverse else range(self.world)
+        return self.t.cat([parts[r] for r in order], 0).contiguous()
 
-        def gathered(x):
-            parts = self._allgather(x).view(self.world, *x.shape)
-            return t.cat([parts[r] for r in order], 0).contiguous()
-
-        Wg = gathered(st.W.index_select(0, idx))
-        bg = None if adj else gathered(st.b.index_select(0, idx))
-        Dg = gathered(lev.adjoint_D.index_select(0, idx)) if adj else None
-        loc = lev.desc()
-        d = _lib.LmgSystem()
-        ctypes.memmove(ctypes.byref(d), ctypes.byref(loc), ctypes.sizeof(d))  # kind, act, step, geometry
-        d.num_layers = n * self.world
-        d.W, d.w_stride = Wg.data_ptr(), Wg[0].numel()
-        if adj:
-            d.b, d.b_stride = None, 0
-            d.D, d.d_stride = Dg.data_ptr(), Dg[0].numel()
-        else:
-            d.b, d.b_stride = bg.data_ptr(), bg[0].numel()
-        self._gsys = (Wg, bg, Dg, d)  # keep the gathered tensors alive with the descriptor
-        return self._gsys
-
-    def _coarsest_gather(self, l, V, SH):
-        lev = self.levels[l]
-        n, t = lev.L, self.t
-        desc = self._global_coarse_system(l)[3]
-        # S_H rows in SYSTEM order: rank order forward, reversed rank order for the adjoint
-        parts = self._allgather(SH[:n]).view(self.world, n, self.B, lev.q)
-        order = range(self.world - 1, -1, -1) if self.reverse else range(self.world)
-        SHg = t.cat([parts[r] for r in order], 0)
-        Vg = t.empty_like(SHg)
-        # every rank runs the same serial solve (the first rank's result is what the reference's
-        # single process computes; running it everywhere replaces the scatter by local slicing)
-        _lib.call("lmg_sequential_forward", desc, self.B, SHg.data_ptr(), _lib.SRC_DENSE,
-                  Vg.data_ptr(), self.ops._st())
+    def _gathered_level(self, l, V, SH):
+        """Level l and below collapsed onto every rank: gather S_H (and
+        the injected initial iterate V when l is not the coarsest), run the sub-hierarchy's
+        exact solve / one FAS cycle on every rank -- the first rank's result is what the
+        reference's single process computes; running it everywhere replaces the scatter by local
+        slicing -- and keep this rank's rows."""
+        n = self.levels[l].L
+        if self._gsys is None:
+            self._gsys = self.ops.gather_system(self, l)
+        SHg = self._allgather_ordered(SH[:n])
+        nlev = self.nlevels - l
+        Vg = self._allgather_ordered(V[:n]) if nlev > 1 else self.t.empty_like(SHg)
+        self.ops.subcycle(self._gsys, nlev, self.c, self.B, Vg, SHg)
         V[:n].copy_(Vg[self.pos * n : (self.pos + 1) * n])
 
     # -- one FAS cycle at level l (multigrid.py:175-228) --------------------------------------
@@ -388,7 +427,7 @@ class DistSolver:
         coarsest = l + 1 == self.nlevels - 1
         ops.coarse_source(lev, U, S, smode, P, None if self.is_first else self.recv2[1],
                           self.is_first, SHn, None if coarsest else Vn, self.advH[l])
-        if coarsest:
+        if l + 1 == self.gather_level:
             self._coarsest(l + 1, Vn, SHn)
         else:
             self.cycle(l + 1, Vn, SHn, _lib.SRC_DENSE, False)
