@@ -290,25 +290,6 @@ class ClockSampler:
                     reasons=sorted(reasons), samples=len(sm))
 
 
-def fp64_peak_tflops(torch, dev):
-    """Measured FP64 tensor peak of this GPU: cuBLAS DGEMM 8192^3 (best of 3, CUDA events).
-    MEASURED_PEAKS.json carries HBM and bf16 only ('measure DGEMM on the box')."""
-    n = 8192
-    a = torch.randn(n, n, dtype=torch.float64, device=dev)
-    b = torch.randn(n, n, dtype=torch.float64, device=dev)
-    torch.matmul(a, b)
-    best = 0.0
-    for _ in range(3):
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        torch.matmul(a, b)
-        e.record()
-        e.synchronize()
-        best = max(best, 2.0 * n ** 3 / (s.elapsed_time(e) * 1e-3) / 1e12)
-    del a, b
-    return best
-
-
 def load_traffic(config):
     """dram bytes per launch of the dominant kernel from the committed ncu --set full summary
     (only when that capture was taken on this config)."""
@@ -346,22 +327,13 @@ class ThetaSnapshot:
         self.torch.cuda.synchronize()
 
 
-def hbm_peak():
-    """(GB/s, source): MEASURED_PEAKS.json (driver-measured on this pool), else the profiling
-    recipe's fallback."""
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"
-    except (OSError, ValueError, KeyError):
-        return 6650.0, "fallback 6.65 TB/s of B200_PROFILING.md (MEASURED_PEAKS.json absent)"
-
-
 def run_ours(args, cfg):
     import numpy as np
     import torch
 
     import paper_2007_07336_b200 as P
     from paper_2007_07336_b200 import _lib
+    from paper_2007_07336_b200.roofline import classify, fp64_peak_tflops, hbm_peak
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -541,16 +513,14 @@ def run_ours(args, cfg):
     gemm_flops = f_flops + a_flops
     gemm_bytes = f_bytes + a_bytes
     hbm, hbm_src = hbm_peak()
-    intensity = gemm_flops / gemm_bytes if gemm_bytes else float("inf")
-    ridge = peak * 1e12 / (hbm * 1e9)
-    if conv or intensity >= ridge:
-        bound, unit_r, pk, pk_src = "tensor", "TFLOP/s", peak, (
-            "cuBLAS DGEMM 8192^3 measured in this run (FP64 is not in MEASURED_PEAKS.json)")
-        achieved = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else 0.0
+    rf = classify(gemm_flops, gemm_bytes, gemm_ms, peak, hbm, force_tensor=conv)
+    bound, unit_r, pk, achieved = rf["bound"], rf["unit"], rf["peak"], rf["achieved"]
+    intensity, ridge = rf["intensity_flop_per_byte"], rf["fp64_ridge_flop_per_byte"]
+    if bound == "tensor":
+        pk_src = "cuBLAS DGEMM 8192^3 measured in this run (FP64 is not in MEASURED_PEAKS.json)"
         alg = "(2q^2+5q) flops per F-evaluation x B samples x tasks per launch"
     else:
-        bound, unit_r, pk, pk_src = "hbm", "GB/s", hbm, hbm_src
-        achieved = gemm_bytes / (gemm_ms * 1e-3) / 1e9 if gemm_ms > 0 else 0.0
+        pk_src = hbm_src
         alg = ("8q^2 (W_j, read once per layer step for the whole batch) + 8qB per state row read "
                "or written, per task, summed over the launches")
     traffic, prof = load_traffic(args.config)

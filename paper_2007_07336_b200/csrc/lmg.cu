@@ -317,9 +317,25 @@ __global__ void k_conv_bias_grads(const double* __restrict__ lam_top, int64_t la
   }
 }
 
+// SM count of the current device (148 on B200), queried once per device: grid sizing, the
+// single-wave test for programmatic dependent launch, tile and split-K choices
+int num_sms() {
+  static std::mutex mu;
+  static std::vector<std::pair<int, int>> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& kv : cache)
+    if (kv.first == dev) return kv.second;
+  int n = 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+  cache.emplace_back(dev, n);
+  return n;
+}
+
 int grid_for(int64_t total) {
   int64_t g = (total + 255) / 256;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)num_sms() * 16));
 }
 
 // ------------------------------------------------------------------------------------------
@@ -441,7 +457,7 @@ int launch_cfg(const StepArgs& a, cudaStream_t st) {
   // multi-wave grids: opt-in (LMG_PDL_MULTI=1), with the trigger after the mainloop -- measured
   // within noise on c2 (1068 vs 1066-1125 ms per step)
   static const bool pdl_multi = getenv("LMG_PDL_MULTI") != nullptr;
-  const bool single = (int64_t)grid.x * grid.y * grid.z <= (int64_t)per_sm * 148;
+  const bool single = (int64_t)grid.x * grid.y * grid.z <= (int64_t)per_sm * num_sms();
   const bool pdl = pdl_on && (single || pdl_multi);
   route(std::is_same<T, TTiny>::value ? (FULL ? LMG_ROUTE_STEP_TINY_FULL : LMG_ROUTE_STEP_TINY)
         : std::is_same<T, TWide>::value ? (FULL ? LMG_ROUTE_STEP_WIDE_FULL : LMG_ROUTE_STEP_WIDE)
@@ -502,7 +518,7 @@ int choose_tile(const StepArgs& a) {
   // parameter gradients of a small batch (K = B <= 32): one k-tile per CTA, so the 32 x 32 grid
   // is launch/epilogue-bound; 32 x 64 tiles halve the CTAs (c5: 2.08 -> 1.85 ms per step)
   if (!AK && a.K <= 32) return SEL_WIDE;
-  if (adj && ctas_for(a, TWide::BM, TWide::BN) >= 2 * 148) return SEL_WIDE;
+  if (adj && ctas_for(a, TWide::BM, TWide::BN) >= 2 * num_sms()) return SEL_WIDE;
   return SEL_SMALL;
 }
 
@@ -563,7 +579,7 @@ int launch_serial(Layout L, const StepArgs& a, cudaStream_t st) {
   if (a.M % BM || a.N % BN || a.K % BK) return -1;
   const int64_t base = (int64_t)(a.N / BN) * (a.M / BM);
   int KS = 1;
-  while (KS < 8 && base * KS * 2 <= 4 * 148 && (a.K / BK) % (KS * 2) == 0) KS *= 2;
+  while (KS < 8 && base * KS * 2 <= 4 * num_sms() && (a.K / BK) % (KS * 2) == 0) KS *= 2;
   if (KS == 1) return -1;
   const bool adj = (L == L_ADJ);
   if (tiny)

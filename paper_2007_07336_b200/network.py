@@ -148,6 +148,7 @@ class ResidualNetwork:
             raise DimensionError(
                 f"readout expects width {self.readout.input_width}, network width is {q}")
         self._device = None
+        self._host_ref, self._block_ids = [], []
 
     @property
     def num_blocks(self) -> int:
@@ -159,12 +160,43 @@ class ResidualNetwork:
 
     # -- device mirror ------------------------------------------------------------------
     def device_stack(self) -> DeviceStack:
-        """The device copy of the block parameters (built on first use).  Host-side edits of
-        ``blocks[i].weights`` after that need `invalidate_device()`; device-side training updates
-        the stack in place and `pull_from_device()` copies it back."""
-        if self._device is None:
-            self._device = DeviceStack.from_blocks(self.blocks)
+        """The device copy of the block parameters, kept in sync with the host arrays.
+
+        The reference edits parameters in place and never rebuilds anything (multigrid.py:83-85,
+        training.py:231; its finite-difference tests perturb ``flat[i]`` and re-evaluate), so
+        every use compares the host arrays with the copy taken at the last upload and re-uploads
+        exactly the blocks that changed (or rebuilds when the block list changed).  Device-side
+        training updates the stack in place; `pull_from_device()` copies it back to the host
+        arrays (and re-bases the comparison copy)."""
+        blocks = self.blocks
+        if self._device is None or len(self._host_ref) != len(blocks) or any(
+                a is not blk for a, blk in zip(self._block_ids, blocks)):
+            self._device = DeviceStack.from_blocks(blocks)
+            self._snapshot()
+            return self._device
+        stale = [i for i, blk in enumerate(blocks)
+                 if not (np.array_equal(blk.weights, self._host_ref[i][0])
+                         and np.array_equal(blk.bias, self._host_ref[i][1]))]
+        if stale:
+            t = require_cuda()
+            if any(np.shape(blocks[i].weights) != self._host_ref[i][0].shape for i in stale):
+                self._device = DeviceStack.from_blocks(blocks)
+                self._snapshot()
+                return self._device
+            idx = t.tensor(stale, device=self._device.W.device)
+            W = np.stack([np.asarray(blocks[i].weights, dtype=np.float64) for i in stale])
+            b = np.stack([np.asarray(blocks[i].bias, dtype=np.float64) for i in stale])
+            self._device.W.index_copy_(0, idx, t.from_numpy(W).to(self._device.W.device))
+            self._device.b.index_copy_(0, idx, t.from_numpy(b).to(self._device.b.device))
+            for i in stale:
+                self._host_ref[i] = (np.array(blocks[i].weights, dtype=np.float64, copy=True),
+                                     np.array(blocks[i].bias, dtype=np.float64, copy=True))
         return self._device
+
+    def _snapshot(self):
+        self._block_ids = list(self.blocks)
+        self._host_ref = [(np.array(blk.weights, dtype=np.float64, copy=True),
+                           np.array(blk.bias, dtype=np.float64, copy=True)) for blk in self.blocks]
 
     def invalidate_device(self):
         self._device = None
@@ -177,6 +209,7 @@ class ResidualNetwork:
         for i, blk in enumerate(self.blocks):
             blk.weights[...] = W[i]
             blk.bias[...] = b[i]
+        self._snapshot()
 
     def _lmg_view(self) -> SystemView:
         return SystemView(self.device_stack(), 1, self.step_size, self.num_blocks)

@@ -239,7 +239,8 @@ def loss_and_grad(net, states, sample, label):
     X = t.from_numpy(np.asarray(sample, dtype=np.float64).ravel()[None]).cuda()
     labels = t.tensor([int(label)], device=X.device)
     r = backward(dnet, st.t, X, labels, adjoint="sequential")
-    blocks = [(r.gW[i].cpu().numpy(), r.gb[i].cpu().numpy()) for i in range(view.n)]
+    gW, gb = r.gW.cpu().numpy(), r.gb.cpu().numpy()  # one bulk copy each
+    blocks = [(gW[i], gb[i]) for i in range(view.n)]
     return float(r.loss[0]), Gradients((r.gWo.cpu().numpy(), r.gbo.cpu().numpy()), blocks,
                                        (r.gWr.cpu().numpy(), r.gbr.cpu().numpy()))
 
@@ -269,26 +270,30 @@ def forward_states(net, sample, cfg: TrainConfig, hierarchy: MgHierarchy | None)
 
 def train_epoch(net: ResidualNetwork, data: Dataset, cfg: TrainConfig, rng=None,
                 hierarchy: MgHierarchy | None = None) -> EpochStats:
-    """training.py:255-289: one SGD epoch over shuffled batches, in place.  Each batch's forward
-    solves and adjoints run as one batched device computation (samples are independent)."""
-    from .network import source_from_input
+    """training.py:255-289: one SGD epoch over shuffled batches, in place.
 
+    Device-resident: the parameters are uploaded once, every batch runs its forward solves, the
+    sequential adjoint (training.py:194-227) and the batch-mean SGD step (training.py:230-236,
+    fused into the parameter-gradient kernel for the blocks) on the device, and the updated
+    parameters are copied back into the host arrays once at the end.  Losses and hits stay on the
+    device until then (one read-back per epoch)."""
     if rng is None:
         rng = np.random.default_rng(cfg.seed)
     if cfg.mode == "mg" and hierarchy is None:
         hierarchy = build_hierarchy(net, cfg.coarsening)
     order = rng.permutation(len(data))
-    losses = np.empty(len(data))
-    hits = 0
     t = require_cuda()
+    dnet = DeviceNet.from_network(net)
+    view = dnet._lmg_view()
+    dev = dnet.Wo.device
+    losses, hits = [], t.zeros((), dtype=t.int64, device=dev)
+    images = data.images.reshape(len(data), -1)
     for lo in range(0, len(order), cfg.batch_size):
         batch = order[lo : lo + cfg.batch_size]
-        X = t.from_numpy(np.stack([data.images[i].ravel() for i in batch])).cuda()
-        labels = t.from_numpy(np.asarray([int(data.labels[i]) for i in batch])).cuda()
-        dnet = DeviceNet.from_network(net)
-        view = dnet._lmg_view()
+        X = t.from_numpy(np.ascontiguousarray(images[batch], dtype=np.float64)).to(dev)
+        labels = t.from_numpy(np.asarray(data.labels[batch], dtype=np.int64)).to(dev)
         f0 = _dense_apply(dnet.Wo, dnet.bo, dnet.open_act, X)
-        U = t.empty((view.n,) + tuple(f0.shape), dtype=t.float64, device=X.device)
+        U = t.empty((view.n,) + tuple(f0.shape), dtype=t.float64, device=dev)
         if cfg.mode == "exact":
             _lib.call("lmg_sequential_forward", view.desc(), U.shape[1], f0.data_ptr(), _lib.SRC_HEAD,
                       U.data_ptr(), _lib.stream_handle())
@@ -296,14 +301,22 @@ def train_epoch(net: ResidualNetwork, data: Dataset, cfg: TrainConfig, rng=None,
             solve_device(view, hierarchy.num_levels, hierarchy.coarsening_factor, f0, U,
                          src_mode=_lib.SRC_HEAD, use_initial=False, tol=cfg.solve_tol,
                          max_cycles=cfg.mg_cycles)
-        r = backward(dnet, U, X, labels, adjoint="sequential", scale=1.0 / len(batch))
-        losses[lo : lo + len(batch)] = r.loss.cpu().numpy()
-        hits += int((r.logits.argmax(dim=1) == labels).sum())
-        grads = Gradients((r.gWo.cpu().numpy() / len(batch), r.gbo.cpu().numpy() / len(batch)),
-                          [(r.gW[i].cpu().numpy(), r.gb[i].cpu().numpy()) for i in range(view.n)],
-                          (r.gWr.cpu().numpy() / len(batch), r.gbr.cpu().numpy() / len(batch)))
-        sgd_update(net, grads, cfg.learning_rate)
-    return EpochStats(float(losses.mean()), 1.0 - hits / len(data))
+        r = backward(dnet, U, X, labels, adjoint="sequential", scale=1.0 / len(batch),
+                     lr=float(cfg.learning_rate), want_grads=False)
+        losses.append(r.loss)
+        hits += (r.logits.argmax(dim=1) == labels).sum()
+    _write_back(net, dnet)
+    loss_all = t.cat(losses).cpu().numpy()
+    return EpochStats(float(loss_all.mean()), 1.0 - int(hits.item()) / len(data))
+
+
+def _write_back(net, dnet) -> None:
+    """Copy the device-updated parameters into the network's host arrays (in place)."""
+    if hasattr(net, "pull_from_device"):
+        net.pull_from_device()
+    for tp, (w, b) in ((net.opening, (dnet.Wo, dnet.bo)), (net.readout, (dnet.Wr, dnet.br))):
+        tp.weights[...] = w.cpu().numpy()
+        tp.bias[...] = b.cpu().numpy()
 
 
 def evaluate(net, data: Dataset) -> float:

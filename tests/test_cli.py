@@ -35,6 +35,18 @@ def test_bad_int_list_exits_2():
     assert cli.main(["converge", "--depths", "8,x"]) == cli.EXIT_CONFIG
 
 
+def test_workers_key_and_flag_like_the_reference(tmp_path):
+    """reference configs carry "workers" (cli.py:42,55,83) and --workers exists."""
+    p = tmp_path / "c.json"
+    p.write_text(json.dumps({"depths": [8], "workers": [2]}))
+    cfg = cli.load_config("converge", _args("converge", config=str(p)))
+    assert cfg["workers"] == [2]
+    cfg = cli.load_config("scale", _args("scale", workers="1,2,4", gpus="1,2"))
+    assert cfg["workers"] == [1, 2, 4] and cfg["gpus"] == [1, 2]
+    assert cli.main(["converge", "--workers", "0"]) == cli.EXIT_CONFIG
+    assert cli.main(["converge", "--gpus", "2"]) == cli.EXIT_CONFIG  # scale only
+
+
 def test_csv_layout(capsys):
     cli.write_rows(None, ["a", "b"], [[1, 0.5]])
     out = capsys.readouterr().out.splitlines()
@@ -52,4 +64,13 @@ def test_commands_on_gpu(tmp_path):
     assert lines[1] == "depth,cycle,residual_l2" and len(lines) > 4
     assert cli.main(["oracle-check", "--depths", "16,64", "--seed", "0", "--out",
                      str(tmp_path / "o.csv")]) == cli.EXIT_OK
-    assert cli.main(["scale", "--batches", "1,4", "--out", str(tmp_path / "s.csv")]) == cli.EXIT_OK
+    s = tmp_path / "s.csv"
+    assert cli.main(["scale", "--batches", "1,4", "--workers", "1,2", "--gpus", "1,2",
+                     "--out", str(s)]) == cli.EXIT_OK
+    lines = s.read_text().splitlines()
+    assert lines[1] == ("workers,gpus,batch,wall_seconds,layer_samples_per_s,bound,roofline_frac,"
+                        "shared,checksum")
+    rows = [ln.split(",") for ln in lines[2:]]
+    assert len(rows) == 6 and {r[1] for r in rows} == {"1", "2"}
+    assert len({r[-1] for r in rows}) == 1  # bitwise across workers, batches and GPU counts
+    assert all(0.0 < float(r[6]) <= 1.0 for r in rows)

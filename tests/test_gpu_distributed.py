@@ -26,6 +26,10 @@ import torch.distributed as dist  # noqa: E402
 import torch.multiprocessing as mp  # noqa: E402
 
 N, Q, B, C, THR = 256, 64, 8, 4, 16  # levels [256, 64, 16]
+SHAPE = (N, C, THR)
+# cf 16, levels [256, 16, 1]: at 8 ranks level 1 does not split into whole blocks, so [16, 1] is
+# gathered onto every rank (distributed.check_partition) -- the c5 hierarchy's situation at 8 GPUs
+SHAPE_C16 = (256, 16, 1)
 
 
 def _port():
@@ -43,7 +47,8 @@ def _inputs():
     return X, np.arange(B) % 10
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, shape=SHAPE):
+    N, C, THR = shape
     sys.path.insert(0, ROOT)
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
@@ -71,7 +76,8 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def _single(rank, out):
+def _single(rank, out, shape=SHAPE):
+    N, C, THR = shape
     sys.path.insert(0, ROOT)
     torch.cuda.set_device(0)
     import paper_2007_07336_b200 as P
@@ -109,9 +115,9 @@ def _spawn(fn, args, nprocs, out, env=None):
         return pickle.load(fh)
 
 
-def _run(world, tmp_path, env=None):
-    out = str(tmp_path / f"w{world}.pkl")
-    return _spawn(_worker, (world, _port(), out), world, out, env)
+def _run(world, tmp_path, env=None, shape=SHAPE):
+    out = str(tmp_path / f"w{world}_{shape[1]}.pkl")
+    return _spawn(_worker, (world, _port(), out, shape), world, out, env)
 
 
 @pytest.mark.parametrize("coarsest", ["gather", "pipeline"])
@@ -131,7 +137,7 @@ def test_partitioned_training_step_bitwise_vs_single_gpu(tmp_path, coarsest):
     assert np.array_equal(ref["cyc"], cyc) and np.array_equal(ref["acyc"], res.adj_cycles)
     assert np.max(np.abs(ref["U"] - U)) <= 1e-12 * max(1.0, np.max(np.abs(U)))
     assert np.max(np.abs(ref["W"] - W1)) <= 1e-12 * max(1.0, np.max(np.abs(W1)))
-    for world in (1, 2, 4):
+    for world in (1, 2, 4, 8):
         r = _run(world, tmp_path, {"LMG_NO_SWEEP": "1", "LMG_COARSEST": coarsest})
         assert r["U"].tobytes() == ref["U"].tobytes(), world
         assert np.array_equal(r["hist"], ref["hist"][: ref["cyc"].max() + 1], equal_nan=True), world
@@ -202,6 +208,24 @@ def test_partitioned_fused_fcf_bitwise(tmp_path):
     for world in (1, 2, 4):
         r = _run(world, tmp_path, env)
         assert r["fused"], world  # the partitioned levels really ran lmg_local_fcf_fused
+        assert r["U"].tobytes() == ref["U"].tobytes(), world
+        assert np.array_equal(r["hist"], ref["hist"][: ref["cyc"].max() + 1], equal_nan=True), world
+        assert np.array_equal(r["ahist"], ref["ahist"][: ref["acyc"].max() + 1], equal_nan=True), world
+        assert r["W"].tobytes() == ref["W"].tobytes(), world
+        assert np.array_equal(r["loss"], ref["loss"]), world
+
+
+def test_collapsed_coarse_levels_bitwise_at_eight_ranks(tmp_path):
+    """cf 16, levels [256, 16, 1] over 8 ranks: the fine level is partitioned (2 blocks per
+    rank), level 1 is gathered and its sub-hierarchy runs on every rank through lmg_mg_cycle --
+    bitwise the single-GPU training step with the same (per-step) kernels."""
+    from paper_2007_07336_b200.distributed import check_partition
+
+    assert check_partition(256, 16, 3, 8) == 1
+    env = {"LMG_NO_SWEEP": "1"}
+    ref = _spawn(_single, (str(tmp_path / "c16.pkl"), SHAPE_C16), 1, str(tmp_path / "c16.pkl"), env)
+    for world in (2, 8):
+        r = _run(world, tmp_path, env, SHAPE_C16)
         assert r["U"].tobytes() == ref["U"].tobytes(), world
         assert np.array_equal(r["hist"], ref["hist"][: ref["cyc"].max() + 1], equal_nan=True), world
         assert np.array_equal(r["ahist"], ref["ahist"][: ref["acyc"].max() + 1], equal_nan=True), world

@@ -39,14 +39,13 @@ def test_finite_difference_gradients():
         for _ in range(2):
             idx = tuple(rng.integers(0, s) for s in param.shape)
             old = param[idx]
+            # the reference's pattern: edit the host array in place and re-evaluate, no rebuild
+            # (the device copy follows host edits, network.ResidualNetwork.device_stack)
             param[idx] = old + eps
-            net.invalidate_device()
             lp = _loss(net, x, label)
             param[idx] = old - eps
-            net.invalidate_device()
             lm = _loss(net, x, label)
             param[idx] = old
-            net.invalidate_device()
             fd = (lp - lm) / (2 * eps)
             assert abs(fd - grad[idx]) <= 1e-5 * max(1e-3, abs(fd)), (idx, fd, grad[idx])
 
@@ -89,3 +88,25 @@ def test_train_epoch_matches_oracle():
     assert np.max(np.abs(net.opening.weights - Wo)) <= 1e-11
     assert np.max(np.abs(net.readout.weights - Wr)) <= 1e-11
     assert abs(stats.mean_loss - float(np.mean(losses))) <= 1e-12
+
+
+def test_host_edits_reach_the_device_copy():
+    """an in-place edit of blocks[i].weights after the first device use must be seen by
+    the next solve (multigrid.py:83-85 aliasing semantics), with only the edited block re-sent."""
+    net = P.random_network(32, 8, [4, 32, 8])
+    f = P.source_from_input(net, P.random_sample(8, 4))
+    s1 = P.sequential_forward(net, f)
+    net.blocks[5].weights *= 1.5
+    net.blocks[9].bias += 0.25
+    s2 = P.sequential_forward(net, f)
+    fresh = P.ResidualNetwork(net.opening, [P.dense_params(b.weights.copy(), b.bias.copy(), b.activation)
+                                            for b in net.blocks], net.readout, net.step_size)
+    s3 = P.sequential_forward(fresh, f)
+    assert not np.array_equal(s1, s2)
+    assert np.array_equal(s2, s3)
+    # device-side updates survive (host unchanged since upload) and are written back on request
+    d = net.device_stack()
+    d.W[3] += 1.0
+    assert np.array_equal(net.device_stack().W[3].cpu().numpy(), net.blocks[3].weights + 1.0)
+    net.pull_from_device()
+    assert np.array_equal(net.device_stack().W.cpu().numpy(), np.stack([b.weights for b in net.blocks]))
