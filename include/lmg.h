@@ -99,6 +99,12 @@ enum {
   LMG_ROUTE_N = 14
 };
 int lmg_route_counts(unsigned long long* out, int n);
+/* Canonical summation order on (1) / off (0, default); returns the previous setting.  On: every
+ * layer step is one k-ascending DMMA chain per output (64-column fused sweeps only, no split-K
+ * serial steps), so states are bitwise independent of batch size, routing and layer partition
+ * -- used by the CLI `scale` checksum (reference cli.py:243-263).  Off: the fastest routing,
+ * equal to the canonical results within the parity tolerance. */
+int lmg_set_canonical_order(int on);
 /* Debug: device buffer (>= 4 u64 per step, or NULL to stop) receiving per-step %globaltimer
  * stamps (step start, state ready, mainloop done, epilogue done) of chain 0 / CTA 0 of every
  * fused persistent sweep launch.  Classes 4/5 of lmg_timing_read are those launches. */

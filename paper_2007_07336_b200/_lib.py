@@ -57,6 +57,7 @@ SIGNATURES = {
     "lmg_launch_count": (ctypes.c_ulonglong, []),
     "lmg_timing_enable": (_I, [_I]),
     "lmg_route_counts": (_I, [ctypes.POINTER(ctypes.c_ulonglong), _I]),
+    "lmg_set_canonical_order": (_I, [_I]),
     "lmg_debug_sweep_trace": (_I, [_P]),
     "lmg_debug_sweep_clusters": (_I, [_I, _I, _I]),
     "lmg_timing_read": (_I, [_I, c_double_p, c_double_p, c_double_p,
@@ -154,6 +155,11 @@ def launch_count() -> int:
 ROUTES = ("step_small", "step_small_full", "step_wide", "step_wide_full", "step_tiny",
           "step_tiny_full", "tgemm_big", "tgemm_small", "serial_splitk", "sweep_fcf", "sweep_seq",
           "conv_fwd", "conv_adj", "conv_pgrad")
+
+
+def set_canonical_order(on: bool) -> bool:
+    """Canonical summation order on/off (include/lmg.h); returns the previous setting."""
+    return bool(load().lmg_set_canonical_order(1 if on else 0))
 
 
 def route_counts() -> dict:

@@ -32,6 +32,11 @@
 #include "lmg_sweep.cuh"
 #include "lmg_tgemm.cuh"
 
+namespace lmg {
+std::atomic<int> g_canonical{0};  // lmg_set_canonical_order
+bool canonical_order() { return g_canonical.load(std::memory_order_relaxed) != 0; }
+}  // namespace lmg
+
 using namespace lmg;
 
 namespace {
@@ -554,13 +559,18 @@ int launch_serial_cfg(const StepArgs& a, int KS, cudaStream_t st) {
   cfg.blockDim = dim3(C::NTHREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 1;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = KS;
+  // serial steps are single-wave chains: programmatic dependent launch overlaps the next step's
+  // launch and weight prefetch with this step's tail (LMG_NO_PDL=1 disables)
+  static const bool pdl_on = getenv("LMG_NO_PDL") == nullptr;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_on ? 2 : 1;
   const int cls = CLS_SERIAL;
   const double flops = (double)a.M * a.N * (2.0 * a.K + 5.0);
   const double bytes = 8.0 * ((double)a.N * a.K + (double)a.M * a.K + 2.0 * a.M * a.N);
@@ -570,7 +580,8 @@ int launch_serial_cfg(const StepArgs& a, int KS, cudaStream_t st) {
 
 // returns LMG_OK after launching, or -1 if the step is not eligible (caller falls back)
 int launch_serial(Layout L, const StepArgs& a, cudaStream_t st) {
-  if (getenv("LMG_NO_SPLITK")) return -1;
+  static const bool off = getenv("LMG_NO_SPLITK") != nullptr;
+  if (off || canonical_order()) return -1;
   if (a.ntasks != 1 || (a.epi != E_PROP && a.epi != E_ADV) || L == L_PG) return -1;
   if (!aligned16(a.A) || !aligned16(a.Bm) || !aligned16(a.Ds) || (a.lda | a.ldb | a.K | a.N) & 1)
     return -1;
@@ -1456,6 +1467,11 @@ extern "C" {
 int lmg_abi_version(void) { return 1; }
 
 unsigned long long lmg_launch_count(void) { return g_launches.load(); }
+
+int lmg_set_canonical_order(int on) {
+  const int prev = lmg::g_canonical.exchange(on ? 1 : 0);
+  return prev;
+}
 
 int lmg_route_counts(unsigned long long* out, int n) {
   if (!out || n < 0) return fail(LMG_ERR_CONFIGURATION, "route counts: bad buffer");

@@ -550,10 +550,22 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     if (ASC) ld_.load_next(base + C::A_SZ);
     lb.load_next(base + C::A_SZ * (ASC ? 2 : 1));
   };
+  // programmatic dependent launch (as step_gemm): the weight stages of this CTA's K slice do not
+  // depend on the previous serial step, so they are fetched before griddepcontrol.wait; the state
+  // (A), the scales and every epilogue operand are read, and everything is written, after it
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s)
+    if (s < KT) lb.load_next(smem + s * C::STAGE + C::A_SZ * (ASC ? 2 : 1));
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(s);
-    cp_commit();
+    if (s < KT) {
+      double* base = smem + s * C::STAGE;
+      la.load_next(base);
+      if (ASC) ld_.load_next(base + C::A_SZ);
+    }
+    cp_commit();  // group 0 also carries the prefetched weight stages
   }
   const int wm0 = wm * C::WTM, wn0 = wn * C::WTN;
   const int fr = lane >> 2, fk = lane & 3;

@@ -487,11 +487,13 @@ cudaError_t launch_c(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
 // SM-us per layer step); a single serial chain -> 1 (twice the SMs on the critical path).
 int sweep_config(int q, int B, int adj, int nchains) {
   (void)B;
-  static const int forced = [] {
+  static const int forced_env = [] {
     const char* e = getenv("LMG_SWEEP_CFG");
     return e ? atoi(e) : -1;
   }();
   const bool ok64 = adj ? fits<Cfg64A>(q) : fits<Cfg64F>(q);
+  if (canonical_order()) return ok64 ? 0 : -1;  // one k-ascending chain or the per-step path
+  const int forced = forced_env;
   const bool ok32 = adj ? fits<Cfg32A>(q) : fits<Cfg32F>(q);
   if (forced == 0 && ok64) return 0;
   if (forced == 1 && ok32) return 1;

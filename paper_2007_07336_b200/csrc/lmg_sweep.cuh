@@ -18,6 +18,11 @@
 
 namespace lmg {
 
+// Canonical summation order (lmg_set_canonical_order): every layer step is one k-ascending DMMA
+// chain per output -- the 64-column sweep configuration only, no split-K serial steps -- so the
+// results are bitwise independent of batch size, partition and routing (defined in lmg.cu).
+bool canonical_order();
+
 enum SweepMode {
   SW_FCF = 0,  // FCF relaxation + the P step of every block (multigrid.py:160-172, :208)
   SW_SEQ = 1   // serial forward substitution rows 1..n-1 (network.py:111-123)

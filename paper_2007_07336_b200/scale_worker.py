@@ -26,9 +26,11 @@ def main() -> None:
     from .distributed import CudaOps, DistSolver
     from .multigrid import _levels_for
     from .network import SystemView
-    from .synthetic import device_network, random_sample
+    from .cli import _samples
+    from .synthetic import device_network
     from .training import _dense_apply
 
+    _lib.set_canonical_order(True)  # the CLI's checksum rows compare bitwise
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
     ap.add_argument("--batch", type=int, required=True)
@@ -54,7 +56,7 @@ def main() -> None:
     solver = DistSolver(view, N, c, nlev, B, rank=rank, world=world, ops=CudaOps(dev), device=dev)
     head = None
     if rank == 0:
-        xs = [random_sample(q, [seed, N, q])] + [random_sample(q, [seed, N, q, b]) for b in range(1, B)]
+        xs = _samples(N, q, seed, B)
         head = _dense_apply(dnet.Wo, dnet.bo, dnet.open_act, torch.from_numpy(np.stack(xs)).to(dev))
     U = torch.zeros(L + 1, B, q, dtype=torch.float64, device=dev)
 
