@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "lmg.h"
+#include "lmg_chain.cuh"
 #include "lmg_conv.cuh"
 #include "lmg_sweep.cuh"
 #include "lmg_tgemm.cuh"
@@ -725,6 +726,178 @@ struct Fam {
   double h2 = 0.0;      // E_PROP + out2: coarse-step advance from the same pre-activation
 };
 
+// the StepArgs of one dense layer-step launch (family() below launches it)
+StepArgs dense_step_args(const lmg_system& S, int B, int epi, const Fam& f) {
+  const int q = S.width;
+  StepArgs a{};
+  a.M = B; a.N = q; a.K = q; a.ntasks = f.ntasks;
+  a.epi = epi; a.h = S.step; a.lr = 0.0; a.scale = 1.0;
+  a.A = f.x; a.A_ts = f.x_ts; a.lda = q;
+  a.Bm = S.W + (int64_t)f.blk0 * S.w_stride; a.B_ts = (int64_t)f.blk_step * S.w_stride; a.ldb = q;
+  a.x = f.x; a.x_ts = f.x_ts;
+  a.s = f.s; a.s_ts = f.s_ts;
+  a.out = f.out; a.out_ts = f.out_ts;
+  a.out2 = f.out2; a.out2_ts = f.out2_ts;
+  a.ldc = q;
+  a.h2 = f.h2;
+  if (is_adjoint(S)) {
+    a.act = LMG_ACT_IDENTITY;
+    a.Ds = S.D + (int64_t)f.blk0 * S.d_stride; a.Ds_ts = (int64_t)f.blk_step * S.d_stride;
+  } else {
+    a.act = S.act;
+    a.bias = S.b ? S.b + (int64_t)f.blk0 * S.b_stride : nullptr;
+    a.bias_ts = (int64_t)f.blk_step * S.b_stride;
+  }
+  return a;
+}
+
+// ---- persistent chain launches (lmg_chain.cuh) ----------------------------------------------
+// A sweep whose step s of task t continues the chain of step s-1 of task t (F sweeps, the C and
+// P steps) runs as ONE cooperative persistent launch with per-(step, task) completion counters
+// instead of one launch per step -- bitwise the same arithmetic.  Used for batches of at most
+// 16 (the HBM-bound regime, where per-step launch ramps and tails cost most); LMG_NO_CHAIN=1
+// disables, LMG_CHAIN_ALL=1 extends it to every fully tiled batch.
+
+struct ChainBuf {
+  int dev;
+  cudaStream_t st;
+  unsigned* flags;
+  size_t n;
+};
+std::mutex g_chain_mu;
+std::vector<ChainBuf> g_chain_bufs;
+
+// per-(device, stream) completion counters: launches on one stream are ordered, concurrent
+// streams get their own.  Allocated outside stream capture only (the first cycle of every solve
+// runs eagerly); a capture that would need a new or bigger buffer falls back to per-step launches
+unsigned* chain_flags(cudaStream_t st, size_t n) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_chain_mu);
+  for (auto& b : g_chain_bufs)
+    if (b.dev == dev && b.st == st) {
+      if (b.n >= n) return b.flags;
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(st, &cs);
+      if (cs != cudaStreamCaptureStatusNone) return nullptr;
+      cudaStreamSynchronize(st);  // the old buffer may still be in use by this stream
+      cudaFree(b.flags);
+      b.flags = nullptr;
+      b.n = 0;
+      if (cudaMalloc(&b.flags, n * sizeof(unsigned)) != cudaSuccess) return nullptr;
+      b.n = n;
+      return b.flags;
+    }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs != cudaStreamCaptureStatusNone) return nullptr;
+  unsigned* f = nullptr;
+  if (cudaMalloc(&f, n * sizeof(unsigned)) != cudaSuccess) return nullptr;
+  g_chain_bufs.push_back(ChainBuf{dev, st, f, n});
+  return f;
+}
+
+template <class T, bool BKM, bool ASC>
+int launch_chain_cfg(const ChainArgs& ca, cudaStream_t st) {
+  using C = GemmCfg<T, true, BKM, ASC>;
+  auto kern = chain_gemm<T, true, BKM, ASC>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (attr != cudaSuccess) return fail(LMG_ERR_CUDA, cudaGetErrorString(attr));
+  static const int per_sm = [] {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, chain_gemm<T, true, BKM, ASC>, C::NTHREADS, C::SMEM);
+    return n;
+  }();
+  if (per_sm < 1) return -1;
+  const int grid = (int)std::min<int64_t>(ca.total, (int64_t)per_sm * num_sms());
+  CUDA_TRY(cudaMemsetAsync(ca.flags, 0, (size_t)ca.nsteps * ca.max_tasks * sizeof(unsigned), st));
+  double flops = 0.0, bytes = 0.0;
+  for (int s = 0; s < ca.nsteps; ++s) {
+    const double nt = ca.st[s].ntasks;
+    flops += nt * ((double)ca.a.M * ca.a.N * (2.0 * ca.a.K + 5.0));
+    bytes += 8.0 * nt * ((double)ca.a.N * ca.a.K + (double)ca.a.M * ca.a.K + 2.0 * ca.a.M * ca.a.N);
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid, 1, 1);
+  lc.blockDim = dim3(C::NTHREADS, 1, 1);
+  lc.dynamicSmemBytes = C::SMEM;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the counters cannot deadlock
+  at[0].val.cooperative = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  route(LMG_ROUTE_CHAIN);
+  return launch(ASC ? CLS_GEMM_ADJ : CLS_GEMM_FWD, flops, bytes, st,
+                [&] { cudaLaunchKernelEx(&lc, kern, ca); });
+}
+
+bool chain_disabled() {
+  static const bool v = getenv("LMG_NO_CHAIN") != nullptr;
+  return v;
+}
+bool chain_all() {
+  static const bool v = getenv("LMG_CHAIN_ALL") != nullptr;
+  return v;
+}
+
+// one chain launch of the steps `fams` (step s of task t reads what step s-1 of task t wrote);
+// war_last: the last step overwrites the row step 0 of the next task reads.  -1: not eligible
+int chain_steps(const lmg_system& S, int B, const Fam* fams, int nsteps, bool war_last, cudaStream_t st) {
+  if (chain_disabled() || is_conv(S) || nsteps < 2 || nsteps > kChainMaxSteps) return -1;
+  if (B > 16 && !chain_all()) return -1;
+  const bool tiny = B <= 16;
+  const int BM = tiny ? TTiny::BM : TSmall::BM, BN = tiny ? TTiny::BN : TSmall::BN, BK = 16;
+  const int q = S.width;
+  if (B % BM || q % BN || q % BK || (q & 1)) return -1;
+  const bool adj = is_adjoint(S);
+  ChainArgs ca{};
+  ca.a = dense_step_args(S, B, E_PROP, fams[0]);
+  ca.nsteps = nsteps;
+  ca.ntn = q / BN;
+  ca.tiles = ca.ntn * (B / BM);
+  ca.war_last = war_last ? 1 : 0;
+  int total = 0, max_tasks = 0;
+  for (int s = 0; s < nsteps; ++s) {
+    const StepArgs a = dense_step_args(S, B, E_PROP, fams[s]);
+    if (a.ntasks <= 0 || a.B_ts != ca.a.B_ts || a.bias_ts != ca.a.bias_ts || a.Ds_ts != ca.a.Ds_ts)
+      return -1;
+    if (a.s && ca.a.s && a.s_ts != ca.a.s_ts) return -1;
+    if (a.s && !ca.a.s) { ca.a.s_ts = a.s_ts; }
+    if (a.out2) {
+      if (ca.a.out2 && a.out2_ts != ca.a.out2_ts) return -1;
+      ca.a.out2 = a.out2;
+      ca.a.out2_ts = a.out2_ts;
+    }
+    if (!aligned16(a.A) || !aligned16(a.Bm) || !aligned16(a.Ds) || !aligned16(a.out) ||
+        (a.A_ts | a.B_ts | a.Ds_ts) & 1)
+      return -1;
+    ChainStep& cs = ca.st[s];
+    cs.A = a.A; cs.A_ts = a.A_ts;
+    cs.Ds = a.Ds;
+    cs.Bm = a.Bm;
+    cs.bias = a.bias;
+    cs.s = a.s;
+    cs.out = a.out; cs.out_ts = a.out_ts;
+    cs.out2 = a.out2; cs.h2 = a.h2;
+    cs.ntasks = a.ntasks;
+    cs.item0 = total;
+    total += a.ntasks * ca.tiles;
+    max_tasks = std::max(max_tasks, a.ntasks);
+  }
+  // the WAR guard compares against step 0's tasks; the other steps never have more tasks
+  for (int s = 1; s < nsteps; ++s)
+    if (fams[s].ntasks > fams[0].ntasks && war_last) return -1;
+  ca.total = total;
+  ca.max_tasks = max_tasks;
+  ca.flags = chain_flags(st, (size_t)nsteps * max_tasks);
+  if (!ca.flags) return -1;
+  if (tiny)
+    return adj ? launch_chain_cfg<TTiny, false, true>(ca, st) : launch_chain_cfg<TTiny, true, false>(ca, st);
+  return adj ? launch_chain_cfg<TSmall, false, true>(ca, st) : launch_chain_cfg<TSmall, true, false>(ca, st);
+}
+
 int family(const lmg_system& S, int B, int epi, const Fam& f, cudaStream_t st) {
   if (f.ntasks <= 0) return LMG_OK;
   const int q = S.width;
@@ -1106,7 +1279,11 @@ int local_fcf_a(const lmg_system& S, int B, int c, double* U, const double* src,
     if (c == 2) TRY(copy_rows(U + BQ, c * BQ, Q, BQ, K1, BQ, st));
     s0 = 1;
   }
-  for (int s = s0; s + 1 < c; ++s) {
+  // steps s0..c-1 of every block's chain: F rows s+1 from s, the last one (s = c-1) the C step
+  // writing row (k+1)c -- which block k+1's step 0 reads (old value) when s0 = 0
+  Fam fams[kChainMaxSteps];
+  int nf = 0;
+  for (int s = s0; s < c; ++s) {
     Fam f;
     f.ntasks = K1; f.blk0 = s; f.blk_step = c;
     f.x = U + (int64_t)s * BQ; f.x_ts = c * BQ;
@@ -1115,14 +1292,15 @@ int local_fcf_a(const lmg_system& S, int B, int c, double* U, const double* src,
     }
     f.s = src_fam(src, mode, BQ, s + 1); f.s_ts = c * BQ;
     f.out = U + (int64_t)(s + 1) * BQ; f.out_ts = c * BQ;
-    TRY(family(S, B, E_PROP, f, st));
+    if (nf < kChainMaxSteps) fams[nf] = f;
+    ++nf;
   }
-  Fam f;
-  f.ntasks = K1; f.blk0 = c - 1; f.blk_step = c;
-  f.x = U + (int64_t)(c - 1) * BQ; f.x_ts = c * BQ;
-  f.s = src_fam(src, mode, BQ, c); f.s_ts = c * BQ;
-  f.out = U + (int64_t)c * BQ; f.out_ts = c * BQ;
-  TRY(family(S, B, E_PROP, f, st));
+  const int rc = nf <= kChainMaxSteps ? chain_steps(S, B, fams, nf, s0 == 0, st) : -1;
+  if (rc < 0) {
+    for (int i = 0; i < nf; ++i) TRY(family(S, B, E_PROP, fams[i], st));
+  } else if (rc != LMG_OK) {
+    return rc;
+  }
   if (is_first) TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]
   return LMG_OK;
 }
@@ -1139,13 +1317,42 @@ int local_fcf_b(const lmg_system& S, int B, int c, double* U, const double* src,
   const int nb = S.num_layers / c;
   const int K1 = nb - 1 + (has_next ? 1 : 0);
   // second F sweep; its first step also emits advH[k] = U[kc] + H F_H(U[kc]) for the coarse
-  // source (same weights W_kc and pre-activation as row kc+1, only the step differs)
-  for (int i = 1; i < c; ++i) TRY(f_step(S, B, c, U, src, mode, i, 0, st, advH));
+  // source (same weights W_kc and pre-activation as row kc+1, only the step differs); then the
+  // P step continues every block's chain from its last F row.  One chain launch when eligible.
+  Fam fams[kChainMaxSteps];
+  int nf = 0;
+  for (int i = 1; i < c && nf < kChainMaxSteps; ++i) {
+    Fam f;
+    f.ntasks = nb; f.blk0 = i - 1; f.blk_step = c;
+    f.x = U + (int64_t)(i - 1) * BQ; f.x_ts = c * BQ;
+    f.s = src_fam(src, mode, BQ, i); f.s_ts = c * BQ;
+    f.out = U + (int64_t)i * BQ; f.out_ts = c * BQ;
+    if (advH && i == 1) {
+      f.out2 = advH; f.out2_ts = BQ;
+      f.h2 = S.step * c;
+    }
+    fams[nf++] = f;
+  }
+  const bool chain_p = P && K1 > 0 && nf < kChainMaxSteps;
+  if (chain_p) {
+    Fam f;
+    f.ntasks = K1; f.blk0 = c - 1; f.blk_step = c;
+    f.x = U + (int64_t)(c - 1) * BQ; f.x_ts = c * BQ;
+    f.s = src_fam(src, mode, BQ, c); f.s_ts = c * BQ;
+    f.out = P + BQ; f.out_ts = BQ;
+    fams[nf++] = f;
+  }
+  int rc = (nf == c - (chain_p ? 0 : 1) && c - 1 + (chain_p ? 1 : 0) <= kChainMaxSteps)
+               ? chain_steps(S, B, fams, nf, false, st) : -1;
+  if (rc != LMG_OK && rc >= 0) return rc;
+  const bool chained = rc == LMG_OK;
+  if (!chained)
+    for (int i = 1; i < c; ++i) TRY(f_step(S, B, c, U, src, mode, i, 0, st, advH));
   if (has_next && adv_out && advH) {
     TRY(copy_rows(adv_out, 0, advH + (int64_t)(nb - 1) * BQ, 0, 1, BQ, st));
     adv_out = nullptr;  // done
   }
-  if (P) {
+  if (P && !(chained && chain_p)) {
     Fam f;
     f.ntasks = K1; f.blk0 = c - 1; f.blk_step = c;
     f.x = U + (int64_t)(c - 1) * BQ; f.x_ts = c * BQ;

@@ -63,7 +63,7 @@ struct SwCfg {
   static_assert(BK % (4 * KS) == 0, "k-split must divide the stage");
   static size_t smem(int q) {
     const int cs = q / NC;
-    return sizeof(double) * ((size_t)ST * STAGE + 2 * (size_t)cs * SL + (size_t)NFG * 32 * 4 * (KS - 1) +
+    return sizeof(double) * ((size_t)ST * STAGE + 2 * (size_t)cs * SL + 2 * (size_t)NFG * 32 * 4 * (KS - 1) +
                              (ADJ ? (size_t)SW_BM * NC : 0)) +
            (2 * ST + 2) * sizeof(uint64_t) + 1024;  // + alignment slack
   }
@@ -151,8 +151,8 @@ __global__ void __launch_bounds__(C::NT, 1) sweep_kernel(const __grid_constant__
   const int CS = (int)cl.num_blocks();
   const int rank = (int)cl.block_rank();
   double* Ab = ring + ST * C::STAGE;             // [2][CS][SL]
-  double* red = Ab + 2 * CS * SL;                // [NFG][32][4] k-split partials
-  double* xs = red + NFG * 32 * 4 * (KS - 1);    // [16][NC] adjoint: own slice, unscaled
+  double* red = Ab + 2 * CS * SL;                // [2][NFG][32][4] k-split partials (by step parity)
+  double* xs = red + 2 * NFG * 32 * 4 * (KS - 1);  // [16][NC] adjoint: own slice, unscaled
   uint64_t* full = reinterpret_cast<uint64_t*>(xs + (ADJ ? SW_BM * NC : 0));
   uint64_t* empty = full + ST;
   uint64_t* sready = empty + ST;                 // [2]: peer slices of A[buf] have landed
@@ -316,7 +316,10 @@ __global__ void __launch_bounds__(C::NT, 1) sweep_kernel(const __grid_constant__
     // finishes one m-fragment, summing in fixed order (ks = 0 part + ks = 1 part)
     int i_lo = 0, i_hi = MT;
     if (KS > 1) {
-      double* r = red + (fg * 32 + lane) * 4;
+      // double-buffered by step parity: step s+1's hand-over cannot overwrite the slots the
+      // partner warp reads at step s even without the all-gather's ordering (which racecheck
+      // cannot see through the st.async / mbarrier chain)
+      double* r = red + ((cur * NFG + fg) * 32 + lane) * 4;
       // the fragment this warp hands over: 1 (ks 0) or 0 (ks 1)
       r[2 * ks] = ks == 0 ? acc[MT - 1][0] : acc[0][0];
       r[2 * ks + 1] = ks == 0 ? acc[MT - 1][1] : acc[0][1];

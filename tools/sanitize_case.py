@@ -6,10 +6,14 @@
 
 Cases (and the kernels they route to, asserted through lmg_route_counts):
   tgemm   N 16, q 128, B 64, cf 4     -- warp-specialised TMA step GEMM (adjoint layout; with
-                                         LMG_TGEMM=all also the forward), mbarrier ring
+                                         LMG_TGEMM=all also the forward), mbarrier ring; run
+                                         with LMG_NO_SWEEP=1 (else the fused sweep takes B 64)
   sweep   N 64, q 128, B 16, cf 4     -- fused persistent FCF / serial sweeps: TMA ring, DSMEM
                                          st.async all-gather, cluster barriers
-  splitk  N 16, q 128, B 32, cf 4, levels [16, 4] -- split-K cluster serial steps (DSMEM reduce)
+  splitk  N 16, q 128, B 32, cf 4, levels [16, 4] -- split-K cluster serial steps (DSMEM reduce);
+                                         LMG_NO_SWEEP=1
+  chain   N 64, q 128, B 16, cf 4     -- persistent chain launches (completion counters,
+                                         cooperative grid); LMG_NO_SWEEP=1
 """
 
 import os
@@ -26,7 +30,8 @@ from paper_2007_07336_b200 import _lib  # noqa: E402
 
 CASES = {"tgemm": (16, 128, 64, 4, 4, ("tgemm_big",)),
          "sweep": (64, 128, 16, 4, 4, ("sweep_fcf", "sweep_seq")),
-         "splitk": (16, 128, 32, 4, 4, ("serial_splitk",))}
+         "splitk": (16, 128, 32, 4, 4, ("serial_splitk",)),
+         "chain": (64, 128, 16, 4, 4, ("chain",))}
 
 
 def main():
