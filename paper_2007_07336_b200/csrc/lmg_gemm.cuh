@@ -64,15 +64,120 @@ struct StepArgs {
   int pdl_late;  // programmatic launch trigger after the mainloop (multi-wave grids), not at start
 };
 
+// FP64 tanh for the epilogues (~22 FP64-pipe operations instead of libdevice's ~37: the tanh
+// shares the FP64 pipe with the DMMAs, and was ~11% of the c2 forward step).  Relative error of a
+// few ulp (tests/test_gpu_parity.py pins it against numpy's tanh); NaN propagates, +-inf -> +-1.
+//   tanh(x) = em1 / (em1 + 2),  em1 = e^(2x) - 1 = 2^m * T[j] * (1 + q) - 1
+// with n = rint(x * 128/ln2) = 64 m + j, rh = x - n * ln2/128 (Cody-Waite, |rh| <= ln2/256),
+// T[j] = 2^(j/64) (table as hi + lo), q = e^(2 rh) - 1 (degree-6 Taylor, error < 1e-19
+// relative), em1 = sT (1 + q) - 1 with sT - 1 exact for m = 0 and the table's low part added
+// (em1 cancels to ~1/3 of its terms for small negative x: the hi-only table gave 25 ulp there),
+// and the quotient by a refined reciprocal (rcp.approx + two Newton steps + one correction).
+static __device__ const double2 kTanhExp2[64] = {  // {hi, lo}: 2^(j/64) = hi + lo
+    {0x1.0000000000000p+0, 0x0.0p+0},
+    {0x1.02c9a3e778061p+0, -0x1.19083535b085dp-56},
+    {0x1.059b0d3158574p+0, 0x1.d73e2a475b465p-55},
+    {0x1.0874518759bc8p+0, 0x1.186be4bb284ffp-57},
+    {0x1.0b5586cf9890fp+0, 0x1.8a62e4adc610bp-54},
+    {0x1.0e3ec32d3d1a2p+0, 0x1.03a1727c57b53p-59},
+    {0x1.11301d0125b51p+0, -0x1.6c51039449b3ap-54},
+    {0x1.1429aaea92de0p+0, -0x1.32fbf9af1369ep-54},
+    {0x1.172b83c7d517bp+0, -0x1.19041b9d78a76p-55},
+    {0x1.1a35beb6fcb75p+0, 0x1.e5b4c7b4968e4p-55},
+    {0x1.1d4873168b9aap+0, 0x1.e016e00a2643cp-54},
+    {0x1.2063b88628cd6p+0, 0x1.dc775814a8495p-55},
+    {0x1.2387a6e756238p+0, 0x1.9b07eb6c70573p-54},
+    {0x1.26b4565e27cddp+0, 0x1.2bd339940e9d9p-55},
+    {0x1.29e9df51fdee1p+0, 0x1.612e8afad1255p-55},
+    {0x1.2d285a6e4030bp+0, 0x1.0024754db41d5p-54},
+    {0x1.306fe0a31b715p+0, 0x1.6f46ad23182e4p-55},
+    {0x1.33c08b26416ffp+0, 0x1.32721843659a6p-54},
+    {0x1.371a7373aa9cbp+0, -0x1.63aeabf42eae2p-54},
+    {0x1.3a7db34e59ff7p+0, -0x1.5e436d661f5e3p-56},
+    {0x1.3dea64c123422p+0, 0x1.ada0911f09ebcp-55},
+    {0x1.4160a21f72e2ap+0, -0x1.ef3691c309278p-58},
+    {0x1.44e086061892dp+0, 0x1.89b7a04ef80d0p-59},
+    {0x1.486a2b5c13cd0p+0, 0x1.3c1a3b69062f0p-56},
+    {0x1.4bfdad5362a27p+0, 0x1.d4397afec42e2p-56},
+    {0x1.4f9b2769d2ca7p+0, -0x1.4b309d25957e3p-54},
+    {0x1.5342b569d4f82p+0, -0x1.07abe1db13cadp-55},
+    {0x1.56f4736b527dap+0, 0x1.9bb2c011d93adp-54},
+    {0x1.5ab07dd485429p+0, 0x1.6324c054647adp-54},
+    {0x1.5e76f15ad2148p+0, 0x1.ba6f93080e65ep-54},
+    {0x1.6247eb03a5585p+0, -0x1.383c17e40b497p-54},
+    {0x1.6623882552225p+0, -0x1.bb60987591c34p-54},
+    {0x1.6a09e667f3bcdp+0, -0x1.bdd3413b26456p-54},
+    {0x1.6dfb23c651a2fp+0, -0x1.bbe3a683c88abp-57},
+    {0x1.71f75e8ec5f74p+0, -0x1.16e4786887a99p-55},
+    {0x1.75feb564267c9p+0, -0x1.0245957316dd3p-54},
+    {0x1.7a11473eb0187p+0, -0x1.41577ee04992fp-55},
+    {0x1.7e2f336cf4e62p+0, 0x1.05d02ba15797ep-56},
+    {0x1.82589994cce13p+0, -0x1.d4c1dd41532d8p-54},
+    {0x1.868d99b4492edp+0, -0x1.fc6f89bd4f6bap-54},
+    {0x1.8ace5422aa0dbp+0, 0x1.6e9f156864b27p-54},
+    {0x1.8f1ae99157736p+0, 0x1.5cc13a2e3976cp-55},
+    {0x1.93737b0cdc5e5p+0, -0x1.75fc781b57ebcp-57},
+    {0x1.97d829fde4e50p+0, -0x1.d185b7c1b85d1p-54},
+    {0x1.9c49182a3f090p+0, 0x1.c7c46b071f2bep-56},
+    {0x1.a0c667b5de565p+0, -0x1.359495d1cd533p-54},
+    {0x1.a5503b23e255dp+0, -0x1.d2f6edb8d41e1p-54},
+    {0x1.a9e6b5579fdbfp+0, 0x1.0fac90ef7fd31p-54},
+    {0x1.ae89f995ad3adp+0, 0x1.7a1cd345dcc81p-54},
+    {0x1.b33a2b84f15fbp+0, -0x1.2805e3084d708p-57},
+    {0x1.b7f76f2fb5e47p+0, -0x1.5584f7e54ac3bp-56},
+    {0x1.bcc1e904bc1d2p+0, 0x1.23dd07a2d9e84p-55},
+    {0x1.c199bdd85529cp+0, 0x1.11065895048ddp-55},
+    {0x1.c67f12e57d14bp+0, 0x1.2884dff483cadp-54},
+    {0x1.cb720dcef9069p+0, 0x1.503cbd1e949dbp-56},
+    {0x1.d072d4a07897cp+0, -0x1.cbc3743797a9cp-54},
+    {0x1.d5818dcfba487p+0, 0x1.2ed02d75b3707p-55},
+    {0x1.da9e603db3285p+0, 0x1.c2300696db532p-54},
+    {0x1.dfc97337b9b5fp+0, -0x1.1a5cd4f184b5cp-54},
+    {0x1.e502ee78b3ff6p+0, 0x1.39e8980a9cc8fp-55},
+    {0x1.ea4afa2a490dap+0, -0x1.e9c23179c2893p-54},
+    {0x1.efa1bee615a27p+0, 0x1.dc7f486a4b6b0p-54},
+    {0x1.f50765b6e4540p+0, 0x1.9d3e12dd8a18bp-54},
+    {0x1.fa7c1819e90d8p+0, 0x1.74853f3a5931ep-55}};
+
+__device__ __forceinline__ double fast_tanh(double x) {
+  x = x > 20.0 ? 20.0 : x;  // |tanh| rounds to 1 beyond 19.06; comparisons keep NaN
+  x = x < -20.0 ? -20.0 : x;
+  const double kMagic = 6755399441055744.0;  // 1.5 * 2^52: rint by addition
+  const double k = fma(x, 0x1.71547652b82fep+7, kMagic);  // x * 128/ln2 + magic
+  const double n = k - kMagic;
+  const int ni = __double2loint(k);
+  double rh = fma(-n, 0x1.62e42fefa2000p-8, x);   // x - n * (ln2/128)_hi (exact product)
+  rh = fma(-n, 0x1.9ef35793c7673p-48, rh);        //   - n * (ln2/128)_lo
+  double p = fma(rh, 0x1.6c16c16c16c17p-4, 0x1.1111111111111p-2);  // 4/45, 4/15
+  p = fma(rh, p, 0x1.5555555555555p-1);  // 2/3
+  p = fma(rh, p, 0x1.5555555555555p+0);  // 4/3
+  p = fma(rh, p, 2.0);
+  p = fma(rh, p, 2.0);
+  const double q = rh * p;                // e^(2 rh) - 1
+  const double sc = __hiloint2double((1023 + (ni >> 6)) << 20, 0);  // 2^m
+  const double2 T = __ldg(&kTanhExp2[ni & 63]);
+  const double sT = sc * T.x;  // exact
+  // sT - 1 is exact when m = 0; the table's low part keeps em1 accurate where it cancels
+  const double em1 = fma(sT, q, fma(sc, T.y, sT - 1.0));
+  const double d = em1 + 2.0;
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  y = fma(y, fma(-d, y, 1.0), y);
+  y = fma(y, fma(-d, y, 1.0), y);
+  double t = em1 * y;
+  t = fma(fma(-d, t, em1), y, t);
+  return copysign(t, x);  // odd: keeps the sign of -0.0 (numpy's tanh(-0.0) = -0.0)
+}
+
 __device__ __forceinline__ double act_fwd(int a, double v) {
-  if (a == LMG_ACT_TANH) return tanh(v);
+  if (a == LMG_ACT_TANH) return fast_tanh(v);
   if (a == LMG_ACT_RELU) return (v >= 0.0 || v != v) ? v : 0.0;  // np.maximum(pre, 0.0)
   return v;
 }
 
 __device__ __forceinline__ double act_der(int a, double v) {
   if (a == LMG_ACT_TANH) {
-    double t = tanh(v);
+    double t = fast_tanh(v);
     return __dadd_rn(1.0, -__dmul_rn(t, t));  // 1.0 - t*t, no contraction
   }
   if (a == LMG_ACT_RELU) return v > 0.0 ? 1.0 : 0.0;

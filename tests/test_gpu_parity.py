@@ -280,3 +280,26 @@ def test_split_batch_step_matches_unsplit():
     assert np.array_equal(r1.loss.cpu().numpy(), r2.loss.cpu().numpy())
     assert np.max(np.abs(W1 - W2)) <= 1e-14
     assert np.max(np.abs(Wo1 - Wo2)) <= 1e-14
+
+
+def test_fast_tanh_accuracy():
+    """The epilogue's FP64 tanh (lmg_gemm.cuh fast_tanh) against numpy's (the reference's
+    activation, kernels.py:24-28): a few ulp over the whole range, exact +-1 in the tails, NaN
+    propagated.  Evaluated through apply_transform with an identity weight (pre = u exactly)."""
+    q = 64
+    rng = np.random.default_rng(17)
+    x = np.concatenate([rng.uniform(-25, 25, 20000), rng.normal(0, 1e-3, 4000),
+                        rng.normal(0, 1e-9, 2000), 10.0 ** rng.uniform(-300, -20, 1000),
+                        -(10.0 ** rng.uniform(-300, -20, 1000)), [0.0, -0.0, 19.0, 19.1, 20.0,
+                                                                   -20.0, 700.0, -700.0, 1e300]])
+    x = np.concatenate([x, np.zeros((-len(x)) % q)]).reshape(-1, q)
+    p = P.dense_params(np.eye(q), np.zeros(q), "tanh")
+    got = P.apply_transform(p, x)
+    want = np.tanh(x)
+    ulp = np.abs(got - want) / np.spacing(np.maximum(np.abs(want), np.finfo(float).tiny))
+    assert np.max(ulp) <= 4, float(np.max(ulp))
+    assert np.array_equal(np.sign(got), np.sign(want))
+    big = np.abs(x) >= 19.1
+    assert np.all(np.abs(got[big]) == 1.0)
+    y = P.apply_transform(p, np.full((1, q), np.nan))
+    assert np.all(np.isnan(y))
