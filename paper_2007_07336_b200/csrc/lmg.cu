@@ -130,6 +130,43 @@ __global__ void k_resid_row0(const double* __restrict__ S0, const double* __rest
   if (threadIdx.x == 0 && part) part[slot * B + b] = sh[0];
 }
 
+// Residual of a non-first rank's row 0 (its source row finished with the halo, minus U[0]) summed
+// exactly as the step GEMM's E_RESID epilogue sums that row on one GPU, where it is an interior
+// row: per 32-column tile (TSmall/TTiny: two 16-column warps, lanes fk = 0..3 each holding
+// columns 2fk + {0, 1} and 8 + 2fk + {0, 1} fma-accumulated in that order, then a shfl-xor 1 / 2
+// tree, then the warps in order), tiles summed in order -- so the block partials, and the norms,
+// are bitwise the single-GPU ones whatever the partition (a tree over the row differs in the last
+// bit).  Dense systems (the partitioned path is dense-only).  One thread per sample.
+__global__ void k_resid_row0_tiles(const double* __restrict__ S0, const double* __restrict__ U0,
+                                   double* __restrict__ part, int B, int q) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double* s = S0 + (int64_t)b * q;
+  const double* u = U0 + (int64_t)b * q;
+  double rs = 0.0;
+  for (int t0 = 0; t0 < q; t0 += 32) {
+    double tile = 0.0;
+    for (int wn = 0; wn < 2; ++wn) {
+      double v[4];
+      for (int fk = 0; fk < 4; ++fk) {
+        double acc = 0.0;
+        for (int j = 0; j < 2; ++j)
+          for (int e = 0; e < 2; ++e) {
+            const int n = t0 + wn * 16 + 2 * fk + j * 8 + e;
+            if (n < q) {
+              const double r = __dadd_rn(s[n], -u[n]);
+              acc = fma(r, r, acc);
+            }
+          }
+        v[fk] = acc;
+      }
+      tile += (v[0] + v[1]) + (v[2] + v[3]);
+    }
+    rs += tile;
+  }
+  part[b] = rs;
+}
+
 // norms[b] = sqrt(sum over slots, in slot order) -- deterministic for any launch geometry
 __global__ void k_reduce_norms(const double* __restrict__ part, int64_t nslots, int B,
                                double* __restrict__ norms) {
@@ -1505,9 +1542,17 @@ int local_residual_full_b(const lmg_system& S, int B, int c, const double* U, co
     }));
     s0 = row;
   }
-  TRY(launch(CLS_ELEM, 0.0, 16.0 * BQ, st, [&] {
-    k_resid_row0<<<B, 256, 0, st>>>(s0, U, nullptr, r0part, 0, B, q);
-  }));
+  if (is_first || is_conv(S)) {
+    // the system's row 0: reduced as the single-GPU solve reduces it (residual_full)
+    TRY(launch(CLS_ELEM, 0.0, 16.0 * BQ, st, [&] {
+      k_resid_row0<<<B, 256, 0, st>>>(s0, U, nullptr, r0part, 0, B, q);
+    }));
+  } else {
+    // an interior row of the whole system: the E_RESID tile order (bitwise the one-GPU norm)
+    TRY(launch(CLS_ELEM, 0.0, 16.0 * BQ, st, [&] {
+      k_resid_row0_tiles<<<(B + 127) / 128, 128, 0, st>>>(s0, U, r0part, B, q);
+    }));
+  }
   return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
     k_combine_full<<<(int)(((int64_t)nb * B + 255) / 256), 256, 0, st>>>(rpart, r0part, nb, c, nt, B,
                                                                           block_part);
