@@ -472,7 +472,15 @@ enum Layout { L_FWD = 0, L_ADJ = 1, L_PG = 2 };
 using TSmall = Tile<32, 32, 16, 2, 2, 4>;  // 4 warps of 16x16, ~5 CTAs/SM
 using TWide = Tile<32, 64, 16, 2, 4, 4>;   // 8 warps of 16x16
 using TTiny = Tile<16, 32, 16, 1, 2, 4>;   // batches <= 16: 2 warps of 16x16, no wasted rows
+// Multi-wave step launches (big batches) keep more CTAs resident rather than deeper rings: the
+// other CTAs' mainloops hide a CTA's epilogue (the FP64 tanh) and its single-stage prefetch
+// (tools/tile_probe.cu on the c2 forward step, 256 tasks x 256x512x512, E_PROP tanh: 4 stages /
+// 5 CTAs per SM 27.5 TF/s, 3 / 7 29.0, 2 / 10 30.1; 64 tasks 26.4 -> 28.5).  Adjoint layout
+// (act'-scaled A, MN-major W): 32x64 2 stages 27.7, 32x128 2 stages 28.1 TF/s.
+using TFwd = Tile<32, 32, 16, 2, 2, 2>;
+using TAdj = Tile<32, 128, 16, 2, 4, 2>;
 static_assert(TTiny::BN == TSmall::BN && TTiny::WN == TSmall::WN, "canonical residual partials");
+static_assert(TFwd::BN == TSmall::BN && TFwd::WN == TSmall::WN, "canonical residual partials");
 
 template <class T, bool AK, bool BKM, bool ASC, int VEC, bool FULL = false>
 int launch_cfg(const StepArgs& a, cudaStream_t st) {
@@ -503,7 +511,8 @@ int launch_cfg(const StepArgs& a, cudaStream_t st) {
   const bool single = (int64_t)grid.x * grid.y * grid.z <= (int64_t)per_sm * num_sms();
   const bool pdl = pdl_on && (single || pdl_multi);
   route(std::is_same<T, TTiny>::value ? (FULL ? LMG_ROUTE_STEP_TINY_FULL : LMG_ROUTE_STEP_TINY)
-        : std::is_same<T, TWide>::value ? (FULL ? LMG_ROUTE_STEP_WIDE_FULL : LMG_ROUTE_STEP_WIDE)
+        : (std::is_same<T, TWide>::value || std::is_same<T, TAdj>::value)
+            ? (FULL ? LMG_ROUTE_STEP_WIDE_FULL : LMG_ROUTE_STEP_WIDE)
                                         : (FULL ? LMG_ROUTE_STEP_SMALL_FULL : LMG_ROUTE_STEP_SMALL));
   StepArgs al = a;  // the launched copy carries the trigger placement
   al.pdl_late = single ? 0 : 1;
@@ -577,10 +586,11 @@ int launch_layout(const StepArgs& a, bool v2, cudaStream_t st) {
     return launch_cfg<TTiny, AK, BKM, ASC, 2>(a, st);
   }
   if (sel == SEL_WIDE) {
+    if (AK && !BKM && full(TAdj::BM, TAdj::BN, TAdj::BK)) return launch_cfg<TAdj, AK, BKM, ASC, 2, true>(a, st);
     if (full(TWide::BM, TWide::BN, TWide::BK)) return launch_cfg<TWide, AK, BKM, ASC, 2, true>(a, st);
     return launch_cfg<TWide, AK, BKM, ASC, 2>(a, st);
   }
-  if (full(TSmall::BM, TSmall::BN, TSmall::BK)) return launch_cfg<TSmall, AK, BKM, ASC, 2, true>(a, st);
+  if (full(TFwd::BM, TFwd::BN, TFwd::BK)) return launch_cfg<TFwd, AK, BKM, ASC, 2, true>(a, st);
   return launch_cfg<TSmall, AK, BKM, ASC, 2>(a, st);
 }
 

@@ -130,6 +130,10 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     }
     for (int kt = 0; kt < KT; ++kt) {
       cp_wait<STAGES - 2>();
+      if (ASC) {
+        double* st0 = smem + (kt % STAGES) * C::STAGE;
+        la.scale_own(st0, st0 + C::A_SZ);
+      }
       __syncthreads();
       {
         const int nk = kt + STAGES - 1;
@@ -142,15 +146,13 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
         cp_commit();
       }
       const double* As = smem + (kt % STAGES) * C::STAGE;
-      const double* Dsm = As + C::A_SZ;
       const double* Bs = As + C::A_SZ * (ASC ? 2 : 1);
       double af[2][C::MT], bf[2][C::NTF];
       auto ldfrag = [&](int buf, int kk) {
 #pragma unroll
         for (int i = 0; i < C::MT; ++i) {
           const int o = a_thr + (AK ? i * 8 * LDA_ + kk : kk * LDA_ + i * 8);
-          af[buf][i] = As[o];
-          if (ASC) af[buf][i] = __dmul_rn(af[buf][i], Dsm[o]);
+          af[buf][i] = As[o];  // scaled in place (scale_own)
         }
 #pragma unroll
         for (int j = 0; j < C::NTF; ++j)

@@ -301,6 +301,27 @@ struct Loader {
   __device__ __forceinline__ bool tid_out_of_range(int i) const {
     return (int)(threadIdx.x + i * NT) >= NV;
   }
+  // the adjoint's act' scaling applied once per staged element, by the thread that copied it
+  // (its cp.async data is visible to it after cp.async.wait_group; the CTA barrier that follows
+  // publishes the product): sm[e] *= ds[e] over this thread's vectors of the stage.  Same
+  // __dmul_rn as scaling each fragment at use -- bitwise -- but once per element per CTA instead
+  // of once per warp that reads it (the per-fragment DMULs cost the adjoint ~25% of its DMMA
+  // issue: tools/tile_probe.cu, 23.2 vs 31.9 TF/s unscaled).
+  __device__ __forceinline__ void scale_own(double* sm, const double* ds) const {
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      if (IT * NT > NV && tid_out_of_range(i)) continue;
+      if (VEC == 2) {
+        double2 v = *reinterpret_cast<const double2*>(sm + soff[i]);
+        const double2 d = *reinterpret_cast<const double2*>(ds + soff[i]);
+        v.x = __dmul_rn(v.x, d.x);
+        v.y = __dmul_rn(v.y, d.y);
+        *reinterpret_cast<double2*>(sm + soff[i]) = v;
+      } else {
+        sm[soff[i]] = __dmul_rn(sm[soff[i]], ds[soff[i]]);
+      }
+    }
+  }
   // fully tiled shapes: running per-thread source pointers, advanced by one k-tile per call
   const double* cur[IT];
   __device__ __forceinline__ void init_full() {
@@ -511,6 +532,10 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
 
   for (int kt = 0; kt < KT; ++kt) {
     cp_wait<STAGES - 2>();
+    if (ASC) {
+      double* st0 = smem + (kt % STAGES) * C::STAGE;
+      la.scale_own(st0, st0 + C::A_SZ);
+    }
     __syncthreads();
     {
       int nk = kt + STAGES - 1;
@@ -518,7 +543,6 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
       cp_commit();
     }
     const double* As = smem + (kt % STAGES) * C::STAGE;
-    const double* Dsm = As + C::A_SZ;
     const double* Bs = As + C::A_SZ * (ASC ? 2 : 1);
     double af[2][C::MT], bf[2][C::NTF];
     // per-thread fragment offsets are loop invariant (a_thr / b_thr); only constants vary below
@@ -526,8 +550,7 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
 #pragma unroll
       for (int i = 0; i < C::MT; ++i) {
         const int o = a_thr + (AK ? i * 8 * LDA_ + kk : kk * LDA_ + i * 8);
-        af[buf][i] = As[o];
-        if (ASC) af[buf][i] = __dmul_rn(af[buf][i], Dsm[o]);
+        af[buf][i] = As[o];  // already scaled by act' (ASC: scale_own)
       }
 #pragma unroll
       for (int j = 0; j < C::NTF; ++j) bf[buf][j] = Bs[b_thr + (BKM ? j * 8 * LDB_ + kk : kk * LDB_ + j * 8)];
@@ -679,11 +702,14 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
   const int b_thr = BKM ? (wn0 + fr) * LDB_ + fk : fk * LDB_ + wn0 + fr;
   for (int kt = 0; kt < KT; ++kt) {
     cp_wait<STAGES - 2>();
+    if (ASC) {
+      double* st0 = smem + (kt % STAGES) * C::STAGE;
+      la.scale_own(st0, st0 + C::A_SZ);
+    }
     __syncthreads();
     if (kt + STAGES - 1 < KT) load_stage((kt + STAGES - 1) % STAGES);
     cp_commit();
     const double* As = smem + (kt % STAGES) * C::STAGE;
-    const double* Dsm = As + C::A_SZ;
     const double* Bs = As + C::A_SZ * (ASC ? 2 : 1);
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
@@ -691,8 +717,7 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
 #pragma unroll
       for (int i = 0; i < C::MT; ++i) {
         const int o = a_thr + (AK ? i * 8 * LDA_ + kk : kk * LDA_ + i * 8);
-        af[i] = As[o];
-        if (ASC) af[i] = __dmul_rn(af[i], Dsm[o]);
+        af[i] = As[o];  // scaled in place (scale_own)
       }
 #pragma unroll
       for (int j = 0; j < C::NTF; ++j) bf[j] = Bs[b_thr + (BKM ? j * 8 * LDB_ + kk : kk * LDB_ + j * 8)];

@@ -254,25 +254,27 @@ cudaError_t launch_t(TgParams& prm, cudaStream_t st) {
 
 }  // namespace
 
-// Routing (measured on B200): big batches (M % 64 == 0; tools/gemm_bench.py, 256 tasks x
-// 256x512x512) -- the adjoint layout runs 27.4 TF/s here vs 26.3 in step_gemm, the forward 26.9
-// vs 28.0 (step_gemm's 5 CTAs/SM hide the FP64 tanh epilogue better than 2 persistent CTAs), so
-// big forward steps stay on step_gemm unless LMG_TGEMM=all.  The 16 x 32 small-batch variant
-// (M = 16, the c5 regime) is bitwise too but measured slower than step_gemm's 16-row tiles
-// (c5 fine-level step 3.40 vs 3.76 TB/s), so it only runs with LMG_TGEMM=small.
+// Routing (measured on B200, opt-in since round 2): big batches (M % 64 == 0; 256 tasks x
+// 256x512x512).  Round 1 routed the adjoint layout here (27.4 TF/s vs 26.3 in step_gemm with the
+// act' scaling applied per fragment); once step_gemm scaled each staged element once and ran
+// 2-stage 32 x 128 tiles (lmg.cu TAdj) the whole c2 step was faster there (1018-1024 vs
+// 1037-1050 ms; scaling once per element here too -- a slab pass behind a named barrier plus a
+// proxy fence -- measured slower than the per-fragment DMULs).  LMG_TGEMM=adj routes big adjoint
+// steps here, =all also the forward steps.  The 16 x 32 small-batch variant (M = 16, the c5
+// regime) is bitwise too but measured slower than step_gemm's 16-row tiles (c5 fine-level step
+// 3.40 vs 3.76 TB/s): LMG_TGEMM=small.
 namespace {
 int tile_kind(const StepArgs& a, bool adj) {  // 0: none, 1: big, 2: small
   static const bool off = getenv("LMG_NO_TGEMM") != nullptr;
-  static const int mode = [] {  // 0 default, 1 all, 2 small
+  static const int mode = [] {  // 0 default (off), 1 all, 2 small, 3 adjoint
     const char* e = getenv("LMG_TGEMM");
-    return !e ? 0 : !strcmp(e, "all") ? 1 : !strcmp(e, "small") ? 2 : 0;
+    return !e ? 0 : !strcmp(e, "all") ? 1 : !strcmp(e, "small") ? 2 : !strcmp(e, "adj") ? 3 : 0;
   }();
-  const bool all = mode == 1;
-  if (off || !encoder()) return 0;
+  if (off || mode == 0 || !encoder()) return 0;
   if (a.epi == E_RESID || a.epi == E_PGRAD || a.M <= 0 || a.ntasks <= 0 || a.K % TBK) return 0;
   if (adj && !a.Ds) return 0;
   if (mode == 2 && a.M == 16 && a.N % 32 == 0) return 2;
-  if (a.M % 64 == 0 && a.N % 64 == 0 && (adj || all)) return 1;
+  if (a.M % 64 == 0 && a.N % 64 == 0 && ((adj && mode == 3) || mode == 1)) return 1;
   return 0;
 }
 }  // namespace

@@ -40,7 +40,8 @@ def main():
     np.savez(out, U0=U0, hist=hist, cyc=cyc, U1=U1.cpu().numpy(), lam=lam.cpu().numpy(),
              loss=r.loss.cpu().numpy(), adj_hist=r.adj_hist, adj_cyc=r.adj_cycles,
              W=d.stack.W.cpu().numpy(), b=d.stack.b.cpu().numpy(), Us=Us.cpu().numpy(),
-             launches=np.array(_lib.launch_count()))
+             launches=np.array(_lib.launch_count()),
+             routes=np.array(list(_lib.route_counts().values())))
 
 
 if __name__ == "__main__":

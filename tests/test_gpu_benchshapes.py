@@ -43,9 +43,9 @@ from paper_2007_07336_b200 import _lib  # noqa: E402
 LR = 0.1
 CASES = {  # name: (N, q, B, c, threshold, max_cycles, kernel variants that must run)
     "c5_full": (1024, 512, 16, 16, 4, 50, ("step_tiny_full", "sweep_fcf", "sweep_seq")),
-    "c2_full_2cyc": (1024, 512, 256, 4, 64, 2, ("step_small_full", "tgemm_big", "serial_splitk")),
-    "c2_depth64": (64, 512, 256, 4, 4, 50, ("step_small_full", "tgemm_big", "serial_splitk")),
-    "c4_depth32": (32, 1024, 128, 4, 8, 50, ("step_small_full", "tgemm_big")),
+    "c2_full_2cyc": (1024, 512, 256, 4, 64, 2, ("step_small_full", "step_wide_full", "serial_splitk")),
+    "c2_depth64": (64, 512, 256, 4, 4, 50, ("step_small_full", "step_wide_full", "serial_splitk")),
+    "c4_depth32": (32, 1024, 128, 4, 8, 50, ("step_small_full", "step_wide_full")),
 }
 
 

@@ -76,3 +76,20 @@ def test_fused_sweep_matches_per_step(case, tmp_path):
         for key in ("U0", "hist", "cyc", "U1", "lam", "loss", "adj_hist", "adj_cyc", "W", "b"):
             assert np.array_equal(one[key], off[key], equal_nan=True), key
     assert int(on["launches"]) <= int(off["launches"])  # B > 144: no fused launch applies
+
+
+@pytest.mark.parametrize("case", [(64, 512, 128, 4, 16), (32, 256, 64, 4, 8)],
+                         ids=lambda c: "N%d_q%d_B%d_c%d" % c[:4])
+def test_tma_step_gemm_is_bitwise_the_default_routing(case, tmp_path):
+    """The warp-specialised TMA kernel (opt-in: LMG_TGEMM=all routes every big-batch forward and
+    adjoint step there) against the default step_gemm tiles (2-stage 32x32 forward, 32x128
+    adjoint): the same k-ascending DMMA chain per output, so a whole training step is bitwise."""
+    from paper_2007_07336_b200._lib import ROUTES
+
+    dflt = _run(case, tmp_path, {})
+    tma = _run(case, tmp_path, {"LMG_TGEMM": "all"})
+    assert tma["routes"][ROUTES.index("tgemm_big")] > 0 and dflt["routes"][ROUTES.index("tgemm_big")] == 0
+    if case[2] >= 128:  # multi-wave adjoint steps: the 32x128 tile ran
+        assert dflt["routes"][ROUTES.index("step_wide_full")] > 0
+    for key in ("U0", "hist", "cyc", "U1", "lam", "loss", "adj_hist", "adj_cyc", "W", "b", "Us"):
+        assert np.array_equal(tma[key], dflt[key], equal_nan=True), key
