@@ -479,6 +479,9 @@ using TTiny = Tile<16, 32, 16, 1, 2, 4>;   // batches <= 16: 2 warps of 16x16, n
 // (act'-scaled A, MN-major W): 32x64 2 stages 27.7, 32x128 2 stages 28.1 TF/s.
 using TFwd = Tile<32, 32, 16, 2, 2, 2>;
 using TAdj = Tile<32, 128, 16, 2, 4, 2>;
+// parameter gradients of a small batch (K = B <= 32: one or two k-tiles): deeper rings only cost
+// occupancy (TWide's 4 stages left 3 CTAs/SM for a launch that streams W in and out)
+using TPg = Tile<32, 64, 16, 2, 4, 2>;
 static_assert(TTiny::BN == TSmall::BN && TTiny::WN == TSmall::WN, "canonical residual partials");
 static_assert(TFwd::BN == TSmall::BN && TFwd::WN == TSmall::WN, "canonical residual partials");
 
@@ -511,7 +514,7 @@ int launch_cfg(const StepArgs& a, cudaStream_t st) {
   const bool single = (int64_t)grid.x * grid.y * grid.z <= (int64_t)per_sm * num_sms();
   const bool pdl = pdl_on && (single || pdl_multi);
   route(std::is_same<T, TTiny>::value ? (FULL ? LMG_ROUTE_STEP_TINY_FULL : LMG_ROUTE_STEP_TINY)
-        : (std::is_same<T, TWide>::value || std::is_same<T, TAdj>::value)
+        : (std::is_same<T, TWide>::value || std::is_same<T, TAdj>::value || std::is_same<T, TPg>::value)
             ? (FULL ? LMG_ROUTE_STEP_WIDE_FULL : LMG_ROUTE_STEP_WIDE)
                                         : (FULL ? LMG_ROUTE_STEP_SMALL_FULL : LMG_ROUTE_STEP_SMALL));
   StepArgs al = a;  // the launched copy carries the trigger placement
@@ -587,6 +590,7 @@ int launch_layout(const StepArgs& a, bool v2, cudaStream_t st) {
   }
   if (sel == SEL_WIDE) {
     if (AK && !BKM && full(TAdj::BM, TAdj::BN, TAdj::BK)) return launch_cfg<TAdj, AK, BKM, ASC, 2, true>(a, st);
+    if (!AK && full(TPg::BM, TPg::BN, TPg::BK)) return launch_cfg<TPg, AK, BKM, ASC, 2, true>(a, st);
     if (full(TWide::BM, TWide::BN, TWide::BK)) return launch_cfg<TWide, AK, BKM, ASC, 2, true>(a, st);
     return launch_cfg<TWide, AK, BKM, ASC, 2>(a, st);
   }

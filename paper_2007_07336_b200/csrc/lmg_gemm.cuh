@@ -376,6 +376,42 @@ __device__ __forceinline__ void epilogue(const StepArgs& a, const EpiPtrs& q, do
   const int actk = a.act;
   const double h = a.h;
   const int ldc = a.ldc;
+  if constexpr (EPI == E_PGRAD) {
+    // out (the weights, SGD in place) aliases x: the compiler must keep each W load behind the
+    // previous store, which made this epilogue one HBM round trip per element (c5: 1.8 ms per
+    // gradient launch, 0.36 of HBM).  Every element is read and written by this thread only, so
+    // all loads are issued first, then the updates.
+    double xv[MT][NTF][2], gv[MT][NTF][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NTF; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = mrow0 + i * 8, n = ncol0 + j * 8 + e;
+          const bool in = m < a.M && n < a.N;
+          const int64_t idx = (int64_t)m * ldc + n;
+          xv[i][j][e] = (in && a.lr != 0.0) ? q.X[idx] : 0.0;
+          gv[i][j][e] = (in && a.accum && q.O2) ? q.O2[idx] : 0.0;
+        }
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      rowsq[i] = 0.0;
+#pragma unroll
+      for (int j = 0; j < NTF; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = mrow0 + i * 8, n = ncol0 + j * 8 + e;
+          if (m >= a.M || n >= a.N) continue;
+          const int64_t idx = (int64_t)m * ldc + n;
+          double g = __dmul_rn(__dmul_rn(acc[i][j][e], h), a.scale);
+          if (a.accum && q.O2) g = __dadd_rn(gv[i][j][e], g);
+          if (q.O2) q.O2[idx] = g;
+          if (a.lr != 0.0) q.O[idx] = __dadd_rn(xv[i][j][e], -__dmul_rn(a.lr, g));
+        }
+    }
+    return;
+  } else {
 #pragma unroll
   for (int i = 0; i < MT; ++i) {
     rowsq[i] = 0.0;
@@ -389,13 +425,6 @@ __device__ __forceinline__ void epilogue(const StepArgs& a, const EpiPtrs& q, do
         if (n >= a.N) continue;
         const int64_t idx = (int64_t)m * ldc + n;
         const double accv = acc[i][j][e];
-        if (EPI == E_PGRAD) {
-          double g = __dmul_rn(__dmul_rn(accv, h), a.scale);
-          if (a.accum && q.O2) g = __dadd_rn(q.O2[idx], g);
-          if (q.O2) q.O2[idx] = g;
-          if (a.lr != 0.0) q.O[idx] = __dadd_rn(q.X[idx], -__dmul_rn(a.lr, g));
-          continue;
-        }
         double pre = accv;
         if (q.bias) pre = __dadd_rn(pre, q.bias[n]);
         if (EPI == E_DERIV) {
@@ -430,6 +459,7 @@ __device__ __forceinline__ void epilogue(const StepArgs& a, const EpiPtrs& q, do
         }
       }
     }
+  }
   }
 }
 
