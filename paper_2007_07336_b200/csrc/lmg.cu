@@ -476,9 +476,11 @@ using TTiny = Tile<16, 32, 16, 1, 2, 4>;   // batches <= 16: 2 warps of 16x16, n
 // other CTAs' mainloops hide a CTA's epilogue (the FP64 tanh) and its single-stage prefetch
 // (tools/tile_probe.cu on the c2 forward step, 256 tasks x 256x512x512, E_PROP tanh: 4 stages /
 // 5 CTAs per SM 27.5 TF/s, 3 / 7 29.0, 2 / 10 30.1; 64 tasks 26.4 -> 28.5).  Adjoint layout
-// (act'-scaled A, MN-major W): 32x64 2 stages 27.7, 32x128 2 stages 28.1 TF/s.
+// (act'-scaled A, MN-major W): scaling each fragment at use 23.2 TF/s (32x64), each staged
+// element once 26.5-28.1 (32x64 / 32x128, 2 stages), the products staged from registers
+// (TileR: act' never enters shared memory) at 64x128 30.6 (64 tasks 25.2 -> 29.3); unscaled 30.5.
 using TFwd = Tile<32, 32, 16, 2, 2, 2>;
-using TAdj = Tile<32, 128, 16, 2, 4, 2>;
+using TAdj = TileR<64, 128, 16, 2, 4>;
 // parameter gradients of a small batch (K = B <= 32: one or two k-tiles): deeper rings only cost
 // occupancy (TWide's 4 stages left 3 CTAs/SM for a launch that streams W in and out)
 using TPg = Tile<32, 64, 16, 2, 4, 2>;
@@ -944,8 +946,34 @@ int chain_steps(const lmg_system& S, int B, const Fam* fams, int nsteps, bool wa
   ca.max_tasks = max_tasks;
   ca.flags = chain_flags(st, (size_t)nsteps * max_tasks);
   if (!ca.flags) return -1;
-  if (tiny)
+  if (tiny) {
+    // LMG_CHAIN_TILE (measurement knob): 1 = 16x32 with 4 warps of 16x8, 2 = 16x64 with 4 warps
+    // of 16x16, 3 = 16x32 3 stages, 4 = 16x32 6 stages
+    static const int v = [] {
+      const char* e = getenv("LMG_CHAIN_TILE");
+      return e ? atoi(e) : 0;
+    }();
+    using T1 = Tile<16, 32, 16, 1, 4, 4>;
+    using T2 = Tile<16, 64, 16, 1, 4, 4>;
+    using T3 = Tile<16, 32, 16, 1, 2, 3>;
+    using T4 = Tile<16, 32, 16, 1, 2, 6>;
+    if (v == 2) {
+      if (q % 64) return -1;
+      ca.ntn = q / 64;
+      ca.tiles = ca.ntn * (B / 16);
+      int tot = 0;
+      for (int s = 0; s < nsteps; ++s) {
+        ca.st[s].item0 = tot;
+        tot += ca.st[s].ntasks * ca.tiles;
+      }
+      ca.total = tot;
+      return adj ? launch_chain_cfg<T2, false, true>(ca, st) : launch_chain_cfg<T2, true, false>(ca, st);
+    }
+    if (v == 1) return adj ? launch_chain_cfg<T1, false, true>(ca, st) : launch_chain_cfg<T1, true, false>(ca, st);
+    if (v == 3) return adj ? launch_chain_cfg<T3, false, true>(ca, st) : launch_chain_cfg<T3, true, false>(ca, st);
+    if (v == 4) return adj ? launch_chain_cfg<T4, false, true>(ca, st) : launch_chain_cfg<T4, true, false>(ca, st);
     return adj ? launch_chain_cfg<TTiny, false, true>(ca, st) : launch_chain_cfg<TTiny, true, false>(ca, st);
+  }
   return adj ? launch_chain_cfg<TSmall, false, true>(ca, st) : launch_chain_cfg<TSmall, true, false>(ca, st);
 }
 

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     // weight stages first: they do not depend on the previous step
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st)
-      if (st < KT) lb.load_next(smem + st * C::STAGE + C::A_SZ * (ASC ? 2 : 1));
+      if (st < KT) lb.load_next(smem + st * C::STAGE + C::B_OFF);
     // wait for this task's previous step (all its tiles), and for the WAR guard
     if (tid == 0) {
       if (s > 0) {
@@ -143,12 +143,12 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
           double* base = smem + (nk % STAGES) * C::STAGE;
           la.load_next(base);
           if (ASC) ld_.load_next(base + C::A_SZ);
-          lb.load_next(base + C::A_SZ * (ASC ? 2 : 1));
+          lb.load_next(base + C::B_OFF);
         }
         cp_commit();
       }
       const double* As = smem + (kt % STAGES) * C::STAGE;
-      const double* Bs = As + C::A_SZ * (ASC ? 2 : 1);
+      const double* Bs = As + C::B_OFF;
       double af[2][C::MT], bf[2][C::NTF];
       auto ldfrag = [&](int buf, int kk) {
 #pragma unroll

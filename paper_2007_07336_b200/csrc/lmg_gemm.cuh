@@ -347,6 +347,15 @@ __device__ __forceinline__ double frag(const double* sm, int mn, int k) {
 template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
 struct Tile {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  static constexpr bool RS = false;
+};
+// Register-staged scaled A (the adjoint layout, fully tiled, 2 stages): each thread loads its
+// A and act' vectors of the NEXT k-tile into registers while the DMMAs of this one run, and
+// stores their product into the A stage -- act' never touches shared memory and no pass over
+// the staged tile is needed.  W keeps its cp.async stage.
+template <int BM_, int BN_, int BK_, int WM_, int WN_>
+struct TileR : Tile<BM_, BN_, BK_, WM_, WN_, 2> {
+  static constexpr bool RS = true;
 };
 
 template <class T, bool AK, bool BKM, bool ASC>
@@ -358,7 +367,9 @@ struct GemmCfg {
   static constexpr int MT = WTM / 8, NTF = WTN / 8;   // m8n8 fragments per warp
   static constexpr int A_SZ = TileShape<AK, BM, BK>::SIZE;
   static constexpr int B_SZ = TileShape<BKM, BN, BK>::SIZE;
-  static constexpr int STAGE = A_SZ * (ASC ? 2 : 1) + B_SZ;
+  static constexpr bool RS = ASC && AK && T::RS;  // register-staged scaled A (TileR)
+  static constexpr int B_OFF = A_SZ * ((ASC && !RS) ? 2 : 1);  // W's offset within a stage
+  static constexpr int STAGE = B_OFF + B_SZ;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE * sizeof(double);
 };
 
@@ -504,14 +515,14 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     if (FULL) {  // loads are issued for kt = 0, 1, 2, ... in order
       la.load_next(base);
       if (ASC) ld_.load_next(base + C::A_SZ);
-      lb.load_next(base + C::A_SZ * (ASC ? 2 : 1));
+      lb.load_next(base + C::B_OFF);
       return;
     }
     const int k0 = kt * BK;
     const bool kfull = kfull_all || (k0 + BK <= a.K);
     la.load(base, kt, k0, a.K, kfull);
     if (ASC) ld_.load(base + C::A_SZ, kt, k0, a.K, kfull);
-    lb.load(base + C::A_SZ * (ASC ? 2 : 1), kt, k0, a.K, kfull);
+    lb.load(base + C::B_OFF, kt, k0, a.K, kfull);
   };
 
   // Programmatic dependent launch: when B is the weight stack (forward / adjoint layouts) its
@@ -524,7 +535,7 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       if (s >= KT) break;
-      double* base = smem + s * C::STAGE + C::A_SZ * (ASC ? 2 : 1);
+      double* base = smem + s * C::STAGE + C::B_OFF;
       if (FULL) {
         lb.load_next(base);
       } else {
@@ -535,52 +546,21 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (a.epi != E_PGRAD && !a.pdl_late) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) {
-      double* base = smem + s * C::STAGE;
-      if (FULL) {
-        la.load_next(base);
-        if (ASC) ld_.load_next(base + C::A_SZ);
-        if (!AK) lb.load_next(base + C::A_SZ * (ASC ? 2 : 1));
-      } else {
-        const int k0 = s * BK;
-        const bool kfull = kfull_all || (k0 + BK <= a.K);
-        la.load(base, s, k0, a.K, kfull);
-        if (ASC) ld_.load(base + C::A_SZ, s, k0, a.K, kfull);
-        if (!AK) lb.load(base + C::A_SZ * (ASC ? 2 : 1), s, k0, a.K, kfull);
-      }
-    }
-    cp_commit();  // group 0 also carries the prefetched weight stages
-  }
 
   const int wm0 = wm * C::WTM, wn0 = wn * C::WTN;
   const int fr = lane >> 2, fk = lane & 3;
   constexpr int LDA_ = TileShape<AK, BM, BK>::LD, LDB_ = TileShape<BKM, BN, BK>::LD;
   const int a_thr = pin(AK ? (wm0 + fr) * LDA_ + fk : fk * LDA_ + wm0 + fr);
   const int b_thr = pin(BKM ? (wn0 + fr) * LDB_ + fk : fk * LDB_ + wn0 + fr);
-
-  for (int kt = 0; kt < KT; ++kt) {
-    cp_wait<STAGES - 2>();
-    if (ASC) {
-      double* st0 = smem + (kt % STAGES) * C::STAGE;
-      la.scale_own(st0, st0 + C::A_SZ);
-    }
-    __syncthreads();
-    {
-      int nk = kt + STAGES - 1;
-      if (nk < KT) load_stage(nk % STAGES, nk);
-      cp_commit();
-    }
-    const double* As = smem + (kt % STAGES) * C::STAGE;
-    const double* Bs = As + C::A_SZ * (ASC ? 2 : 1);
+  // the DMMAs of one staged k-tile (fragments double-buffered across the k4 steps)
+  auto compute = [&](const double* As, const double* Bs) {
     double af[2][C::MT], bf[2][C::NTF];
     // per-thread fragment offsets are loop invariant (a_thr / b_thr); only constants vary below
     auto ldfrag = [&](int buf, int kk) {
 #pragma unroll
       for (int i = 0; i < C::MT; ++i) {
         const int o = a_thr + (AK ? i * 8 * LDA_ + kk : kk * LDA_ + i * 8);
-        af[buf][i] = As[o];  // already scaled by act' (ASC: scale_own)
+        af[buf][i] = As[o];  // already scaled by act' (ASC: scale_own / register staging)
       }
 #pragma unroll
       for (int j = 0; j < C::NTF; ++j) bf[buf][j] = Bs[b_thr + (BKM ? j * 8 * LDB_ + kk : kk * LDB_ + j * 8)];
@@ -595,7 +575,82 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
 #pragma unroll
         for (int j = 0; j < C::NTF; ++j) dmma(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
     }
+  };
+
+  if constexpr (C::RS) {
+    static_assert(STAGES == 2 && FULL && VEC == 2, "register staging: 2 stages, fully tiled, 16-byte vectors");
+    constexpr int IT = decltype(la)::IT;
+    double2 ra[IT], rd[IT];
+    auto ldg = [&] {  // this thread's A and act' vectors of the next k-tile
+#pragma unroll
+      for (int i = 0; i < IT; ++i) {
+        if (IT * C::NTHREADS > decltype(la)::NV && la.tid_out_of_range(i)) continue;
+        ra[i] = *reinterpret_cast<const double2*>(la.cur[i]);
+        rd[i] = *reinterpret_cast<const double2*>(ld_.cur[i]);
+        la.cur[i] += la.kadv;
+        ld_.cur[i] += ld_.kadv;
+      }
+    };
+    auto sts = [&](double* base) {  // their products into the A stage (same __dmul_rn: bitwise)
+#pragma unroll
+      for (int i = 0; i < IT; ++i) {
+        if (IT * C::NTHREADS > decltype(la)::NV && la.tid_out_of_range(i)) continue;
+        double2 v;
+        v.x = __dmul_rn(ra[i].x, rd[i].x);
+        v.y = __dmul_rn(ra[i].y, rd[i].y);
+        *reinterpret_cast<double2*>(base + la.soff[i]) = v;
+      }
+    };
+    ldg();
+    sts(smem);
+    cp_commit();  // group 0: the weight stage prefetched before griddepcontrol.wait
+    if (KT > 1) ldg();
+    for (int kt = 0; kt < KT; ++kt) {
+      cp_wait<0>();
+      __syncthreads();  // W stage kt landed and A stage kt stored; stage kt-1 fully consumed
+      double* nxt = smem + ((kt + 1) & 1) * C::STAGE;
+      if (kt + 1 < KT) lb.load_next(nxt + C::B_OFF);
+      cp_commit();
+      compute(smem + (kt & 1) * C::STAGE, smem + (kt & 1) * C::STAGE + C::B_OFF);
+      if (kt + 1 < KT) {
+        sts(nxt);
+        if (kt + 2 < KT) ldg();
+      }
+    }
+  } else {
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < KT) {
+      double* base = smem + s * C::STAGE;
+      if (FULL) {
+        la.load_next(base);
+        if (ASC) ld_.load_next(base + C::A_SZ);
+        if (!AK) lb.load_next(base + C::B_OFF);
+      } else {
+        const int k0 = s * BK;
+        const bool kfull = kfull_all || (k0 + BK <= a.K);
+        la.load(base, s, k0, a.K, kfull);
+        if (ASC) ld_.load(base + C::A_SZ, s, k0, a.K, kfull);
+        if (!AK) lb.load(base + C::B_OFF, s, k0, a.K, kfull);
+      }
+    }
+    cp_commit();  // group 0 also carries the prefetched weight stages
   }
+  for (int kt = 0; kt < KT; ++kt) {
+    cp_wait<STAGES - 2>();
+    if (ASC) {
+      double* st0 = smem + (kt % STAGES) * C::STAGE;
+      la.scale_own(st0, st0 + C::A_SZ);
+    }
+    __syncthreads();
+    {
+      int nk = kt + STAGES - 1;
+      if (nk < KT) load_stage(nk % STAGES, nk);
+      cp_commit();
+    }
+    compute(smem + (kt % STAGES) * C::STAGE, smem + (kt % STAGES) * C::STAGE + C::B_OFF);
+  }
+  }  // register staging / cp.async staging
   cp_wait<0>();
   // multi-wave grids trigger here: the dependent grid launches once every CTA has reached its
   // epilogue, i.e. while the last wave finishes, instead of parking on slots the grid still needs
@@ -619,7 +674,9 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     case E_COARSE_R: epilogue<E_COARSE_R>(a, q, acc, mrow0, ncol0, rowsq); break;
     case E_PROPOP: epilogue<E_PROPOP>(a, q, acc, mrow0, ncol0, rowsq); break;
     case E_DERIV: epilogue<E_DERIV>(a, q, acc, mrow0, ncol0, rowsq); break;
-    case E_PGRAD: epilogue<E_PGRAD>(a, q, acc, mrow0, ncol0, rowsq); break;
+    case E_PGRAD:  // only the parameter-gradient layout (A MN-major) runs it
+      if constexpr (!AK) epilogue<E_PGRAD>(a, q, acc, mrow0, ncol0, rowsq);
+      break;
     case E_APPLY: epilogue<E_APPLY>(a, q, acc, mrow0, ncol0, rowsq); break;
     default: epilogue<E_ADV>(a, q, acc, mrow0, ncol0, rowsq); break;
   }
@@ -706,14 +763,14 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     double* base = smem + s * C::STAGE;
     la.load_next(base);
     if (ASC) ld_.load_next(base + C::A_SZ);
-    lb.load_next(base + C::A_SZ * (ASC ? 2 : 1));
+    lb.load_next(base + C::B_OFF);
   };
   // programmatic dependent launch (as step_gemm): the weight stages of this CTA's K slice do not
   // depend on the previous serial step, so they are fetched before griddepcontrol.wait; the state
   // (A), the scales and every epilogue operand are read, and everything is written, after it
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s)
-    if (s < KT) lb.load_next(smem + s * C::STAGE + C::A_SZ * (ASC ? 2 : 1));
+    if (s < KT) lb.load_next(smem + s * C::STAGE + C::B_OFF);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #pragma unroll
@@ -740,7 +797,7 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     if (kt + STAGES - 1 < KT) load_stage((kt + STAGES - 1) % STAGES);
     cp_commit();
     const double* As = smem + (kt % STAGES) * C::STAGE;
-    const double* Bs = As + C::A_SZ * (ASC ? 2 : 1);
+    const double* Bs = As + C::B_OFF;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[C::MT], bf[C::NTF];

@@ -49,7 +49,8 @@ def main():
         if n == 0:  # routed to the fused sweep (class 4/5)
             ms, fl, _, n = _lib.timing_read(cls + 4)
         _lib.timing_enable(False)
-        return dict(ms_per_launch=ms / n, tflops=fl / (ms * 1e-3) / 1e12, launches=n)
+        return dict(ms_per_launch=ms / n if n else None,
+                    tflops=fl / (ms * 1e-3) / 1e12 if ms > 0 else None, launches=n)
 
     out["sweep"] = timed(lambda: _lib.call("lmg_f_relax", view.desc(), B, 4, U.data_ptr(), S.data_ptr(),
                                            _lib.SRC_HEAD, st), 0)

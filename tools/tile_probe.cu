@@ -104,38 +104,54 @@ int main(int argc, char** argv) {
 
   std::vector<double> ref(nout), tmp(nout);
   const int reps = 10;
-  printf("tasks %d  M %d  N %d  K %d  (E_PROP tanh)\n", tasks, M, N, K);
-  run<Tile<32, 32, 16, 2, 2, 4>>(a, reps, "32x32x16 2x2w 4st (production)", nullptr, nullptr, 0);
-  CK(cudaMemcpy(ref.data(), out, nout * 8, cudaMemcpyDeviceToHost));
-  run<Tile<64, 64, 16, 2, 2, 4>>(a, reps, "64x64x16 2x2w 4st", ref.data(), tmp.data(), nout);
-  run<Tile<64, 64, 16, 2, 2, 3>>(a, reps, "64x64x16 2x2w 3st", ref.data(), tmp.data(), nout);
-  run<Tile<64, 64, 16, 2, 4, 4>>(a, reps, "64x64x16 2x4w 4st", ref.data(), tmp.data(), nout);
-  run<Tile<64, 64, 16, 4, 2, 4>>(a, reps, "64x64x16 4x2w 4st", ref.data(), tmp.data(), nout);
-  run<Tile<128, 64, 16, 4, 2, 3>>(a, reps, "128x64x16 4x2w 3st", ref.data(), tmp.data(), nout);
-  run<Tile<128, 64, 16, 4, 2, 4>>(a, reps, "128x64x16 4x2w 4st", ref.data(), tmp.data(), nout);
-  run<Tile<64, 128, 16, 2, 4, 3>>(a, reps, "64x128x16 2x4w 3st", ref.data(), tmp.data(), nout);
-  run<Tile<128, 128, 16, 4, 2, 3>>(a, reps, "128x128x16 4x2w 3st", ref.data(), tmp.data(), nout);
-  run<Tile<128, 128, 16, 4, 4, 3>>(a, reps, "128x128x16 4x4w 3st", ref.data(), tmp.data(), nout);
-  run<Tile<128, 64, 32, 4, 2, 3>>(a, reps, "128x64x32 4x2w 3st", ref.data(), tmp.data(), nout);
-  run<Tile<64, 32, 16, 2, 2, 4>>(a, reps, "64x32x16 2x2w 4st", ref.data(), tmp.data(), nout);
-  run<Tile<32, 64, 16, 2, 2, 4>>(a, reps, "32x64x16 2x2w 4st", ref.data(), tmp.data(), nout);
-  run<Tile<64, 32, 16, 4, 1, 4>>(a, reps, "64x32x16 4x1w 4st", ref.data(), tmp.data(), nout);
-  // identity activation: the mainloop alone
-  a.act = LMG_ACT_IDENTITY;
-  run<Tile<32, 32, 16, 2, 2, 4>>(a, reps, "identity 32x32x16 (production)", nullptr, nullptr, 0);
-  run<Tile<64, 64, 16, 2, 2, 4>>(a, reps, "identity 64x64x16 2x2w 4st", nullptr, nullptr, 0);
-  run<Tile<128, 64, 16, 4, 2, 3>>(a, reps, "identity 128x64x16 4x2w 3st", nullptr, nullptr, 0);
-  run<Tile<128, 128, 16, 4, 2, 3>>(a, reps, "identity 128x128x16 4x2w 3st", nullptr, nullptr, 0);
-  // adjoint layout: A = mu * D (K-major, scaled), B = W MN-major, identity, no bias
-  a.Ds = S; a.Ds_ts = (int64_t)M * K;
-  CK(cudaMemcpy(S, h.data(), std::min(nout, nw) * 8, cudaMemcpyHostToDevice));
-  a.bias = nullptr; a.s = nullptr;
-  run<Tile<32, 64, 16, 2, 4, 4>, false, true>(a, reps, "adj 32x64x16 2x4w 4st (TWide)", nullptr, nullptr, 0);
-  CK(cudaMemcpy(ref.data(), out, nout * 8, cudaMemcpyDeviceToHost));
-  run<Tile<32, 32, 16, 2, 2, 4>, false, true>(a, reps, "adj 32x32x16 2x2w 4st", ref.data(), tmp.data(), nout);
-  run<Tile<64, 64, 16, 2, 2, 4>, false, true>(a, reps, "adj 64x64x16 2x2w 4st", ref.data(), tmp.data(), nout);
-  run<Tile<128, 64, 16, 4, 2, 3>, false, true>(a, reps, "adj 128x64x16 4x2w 3st", ref.data(), tmp.data(), nout);
-  run<Tile<128, 128, 16, 4, 2, 3>, false, true>(a, reps, "adj 128x128x16 4x2w 3st", ref.data(), tmp.data(), nout);
-  run<Tile<64, 128, 16, 2, 4, 3>, false, true>(a, reps, "adj 64x128x16 2x4w 3st", ref.data(), tmp.data(), nout);
+  const int group = argc > 5 ? atoi(argv[5]) : 0;
+  printf("tasks %d  M %d  N %d  K %d  group %d\n", tasks, M, N, K, group);
+  if (group == 0 || group == 1) {  // forward layout, E_PROP tanh
+    run<Tile<32, 32, 16, 2, 2, 4>>(a, reps, "32x32x16 2x2w 4st (production)", nullptr, nullptr, 0);
+    CK(cudaMemcpy(ref.data(), out, nout * 8, cudaMemcpyDeviceToHost));
+    run<Tile<32, 32, 16, 2, 2, 3>>(a, reps, "32x32x16 2x2w 3st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 32, 16, 2, 2, 2>>(a, reps, "32x32x16 2x2w 2st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 32, 8, 2, 2, 4>>(a, reps, "32x32x8 2x2w 4st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 32, 8, 2, 2, 6>>(a, reps, "32x32x8 2x2w 6st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 32, 8, 2, 2, 2>>(a, reps, "32x32x8 2x2w 2st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 32, 8, 2, 2, 3>>(a, reps, "32x32x8 2x2w 3st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 64, 16, 2, 4, 2>>(a, reps, "32x64x16 2x4w 2st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 32, 32, 2, 2, 2>>(a, reps, "32x32x32 2x2w 2st", ref.data(), tmp.data(), nout);
+    run<Tile<64, 128, 16, 2, 4, 3>>(a, reps, "64x128x16 2x4w 3st", ref.data(), tmp.data(), nout);
+    run<Tile<64, 64, 16, 2, 2, 3>>(a, reps, "64x64x16 2x2w 3st", ref.data(), tmp.data(), nout);
+    a.act = LMG_ACT_RELU;
+    run<Tile<32, 32, 16, 2, 2, 4>>(a, reps, "relu 32x32x16 (production)", nullptr, nullptr, 0);
+    a.act = LMG_ACT_IDENTITY;
+    run<Tile<32, 32, 16, 2, 2, 4>>(a, reps, "identity 32x32x16 (production)", nullptr, nullptr, 0);
+    run<Tile<32, 32, 16, 2, 2, 3>>(a, reps, "identity 32x32x16 3st", nullptr, nullptr, 0);
+    run<Tile<32, 32, 16, 2, 2, 2>>(a, reps, "identity 32x32x16 2st", nullptr, nullptr, 0);
+    run<Tile<64, 128, 16, 2, 4, 3>>(a, reps, "identity 64x128x16 2x4w 3st", nullptr, nullptr, 0);
+    a.act = LMG_ACT_TANH;
+  }
+  if (group == 0 || group == 2) {  // adjoint layout: A = mu * D (K-major, scaled), B = W MN-major
+    a.act = LMG_ACT_IDENTITY;
+    a.Ds = S; a.Ds_ts = (int64_t)M * K;
+    CK(cudaMemcpy(S, h.data(), std::min(nout, nw) * 8, cudaMemcpyHostToDevice));
+    a.bias = nullptr; a.s = nullptr;
+    run<Tile<32, 64, 16, 2, 4, 4>, false, true>(a, reps, "adj 32x64x16 2x4w 4st (TWide)", nullptr, nullptr, 0);
+    CK(cudaMemcpy(ref.data(), out, nout * 8, cudaMemcpyDeviceToHost));
+    run<Tile<32, 64, 16, 2, 4, 3>, false, true>(a, reps, "adj 32x64x16 2x4w 3st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 64, 16, 2, 4, 2>, false, true>(a, reps, "adj 32x64x16 2x4w 2st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 32, 16, 2, 2, 4>, false, true>(a, reps, "adj 32x32x16 2x2w 4st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 32, 16, 2, 2, 2>, false, true>(a, reps, "adj 32x32x16 2x2w 2st", ref.data(), tmp.data(), nout);
+    run<TileR<32, 128, 16, 2, 4>, false, true>(a, reps, "adj RS 32x128x16 2x4w", ref.data(), tmp.data(), nout);
+    run<TileR<32, 64, 16, 2, 4>, false, true>(a, reps, "adj RS 32x64x16 2x4w", ref.data(), tmp.data(), nout);
+    run<TileR<32, 32, 16, 2, 2>, false, true>(a, reps, "adj RS 32x32x16 2x2w", ref.data(), tmp.data(), nout);
+    run<TileR<64, 128, 16, 2, 4>, false, true>(a, reps, "adj RS 64x128x16 2x4w", ref.data(), tmp.data(), nout);
+    run<TileR<32, 128, 8, 2, 4>, false, true>(a, reps, "adj RS 32x128x8 2x4w", ref.data(), tmp.data(), nout);
+    run<Tile<64, 128, 16, 2, 4, 3>, false, true>(a, reps, "adj 64x128x16 2x4w 3st", ref.data(), tmp.data(), nout);
+    run<Tile<64, 128, 16, 2, 4, 2>, false, true>(a, reps, "adj 64x128x16 2x4w 2st", ref.data(), tmp.data(), nout);
+    run<Tile<64, 64, 16, 2, 4, 2>, false, true>(a, reps, "adj 64x64x16 2x4w 2st", ref.data(), tmp.data(), nout);
+    run<Tile<32, 128, 16, 2, 4, 2>, false, true>(a, reps, "adj 32x128x16 2x4w 2st", ref.data(), tmp.data(), nout);
+    // without the act' scaling: what the scaling costs
+    run<Tile<32, 64, 16, 2, 4, 4>, false, false>(a, reps, "adj-noscale 32x64x16 (TWide)", nullptr, nullptr, 0);
+    run<Tile<32, 64, 16, 2, 4, 2>, false, false>(a, reps, "adj-noscale 32x64x16 2st", nullptr, nullptr, 0);
+    run<Tile<64, 128, 16, 2, 4, 3>, false, false>(a, reps, "adj-noscale 64x128x16 2x4w 3st", nullptr, nullptr, 0);
+  }
   return 0;
 }
