@@ -317,7 +317,9 @@ class ThetaSnapshot:
     def __init__(self, torch, dnet):
         self.live = [dnet.stack.W, dnet.stack.b, dnet.Wo, dnet.bo, dnet.Wr, dnet.br]
         need = sum(x.numel() * x.element_size() for x in self.live)
-        where = "cuda" if need < torch.cuda.mem_get_info()[0] // 3 else "cpu"
+        # on the device only when it leaves room for the serial baseline's extra (N, B, q) stacks
+        # (c4 at B 512: theta 32 GiB, each stack 16 GiB)
+        where = "cuda" if need < torch.cuda.mem_get_info()[0] // 8 else "cpu"
         self.saved = [x.detach().to(where, copy=True) for x in self.live]
         self.torch = torch
 

@@ -947,19 +947,20 @@ int chain_steps(const lmg_system& S, int B, const Fam* fams, int nsteps, bool wa
   ca.flags = chain_flags(st, (size_t)nsteps * max_tasks);
   if (!ca.flags) return -1;
   if (tiny) {
-    // LMG_CHAIN_TILE (measurement knob): 1 = 16x32 with 4 warps of 16x8, 2 = 16x64 with 4 warps
-    // of 16x16, 3 = 16x32 3 stages, 4 = 16x32 6 stages
+    // Chain tiles: 16 x 32 with 4 warps of 16 x 8 (the default, 1) -- twice the warps of the
+    // per-step kernel's TTiny at the same shared memory per CTA, which hides the per-k-tile
+    // barrier and the W stream's latency better: c5 relaxation class 0.71 -> 0.78 of HBM, step
+    // 20.6 -> 19.8 ms.  Measured alternatives (LMG_CHAIN_TILE, c5 class fraction of HBM):
+    // 0 = TTiny 2 warps 0.71, 2 = 16x64 4 warps 0.77, 3 / 4 = TTiny 3 / 6 stages 0.68 / 0.64,
+    // 5 = 16x64 8 warps 0.78, 6 = 16x128 8 warps 0.72, 7 = 16x32 4 warps 5 stages 0.77,
+    // 8 = 16x64 8 warps 3 stages 0.73.
     static const int v = [] {
       const char* e = getenv("LMG_CHAIN_TILE");
-      return e ? atoi(e) : 0;
+      return e ? atoi(e) : 1;
     }();
-    using T1 = Tile<16, 32, 16, 1, 4, 4>;
-    using T2 = Tile<16, 64, 16, 1, 4, 4>;
-    using T3 = Tile<16, 32, 16, 1, 2, 3>;
-    using T4 = Tile<16, 32, 16, 1, 2, 6>;
-    if (v == 2) {
-      if (q % 64) return -1;
-      ca.ntn = q / 64;
+    auto retile = [&](int bn) {  // item geometry for a BN-column tile
+      if (q % bn) return false;
+      ca.ntn = q / bn;
       ca.tiles = ca.ntn * (B / 16);
       int tot = 0;
       for (int s = 0; s < nsteps; ++s) {
@@ -967,12 +968,24 @@ int chain_steps(const lmg_system& S, int B, const Fam* fams, int nsteps, bool wa
         tot += ca.st[s].ntasks * ca.tiles;
       }
       ca.total = tot;
-      return adj ? launch_chain_cfg<T2, false, true>(ca, st) : launch_chain_cfg<T2, true, false>(ca, st);
+      return true;
+    };
+    auto go = [&](auto tile) -> int {
+      using T = decltype(tile);
+      if (!retile(T::BN)) return -1;
+      return adj ? launch_chain_cfg<T, false, true>(ca, st) : launch_chain_cfg<T, true, false>(ca, st);
+    };
+    switch (v) {
+      case 0: return go(TTiny{});
+      case 2: return go(Tile<16, 64, 16, 1, 4, 4>{});
+      case 3: return go(Tile<16, 32, 16, 1, 2, 3>{});
+      case 4: return go(Tile<16, 32, 16, 1, 2, 6>{});
+      case 5: return go(Tile<16, 64, 16, 1, 8, 4>{});
+      case 6: return go(Tile<16, 128, 16, 1, 8, 4>{});
+      case 7: return go(Tile<16, 32, 16, 1, 4, 5>{});
+      case 8: return go(Tile<16, 64, 16, 1, 8, 3>{});
+      default: return go(Tile<16, 32, 16, 1, 4, 4>{});
     }
-    if (v == 1) return adj ? launch_chain_cfg<T1, false, true>(ca, st) : launch_chain_cfg<T1, true, false>(ca, st);
-    if (v == 3) return adj ? launch_chain_cfg<T3, false, true>(ca, st) : launch_chain_cfg<T3, true, false>(ca, st);
-    if (v == 4) return adj ? launch_chain_cfg<T4, false, true>(ca, st) : launch_chain_cfg<T4, true, false>(ca, st);
-    return adj ? launch_chain_cfg<TTiny, false, true>(ca, st) : launch_chain_cfg<TTiny, true, false>(ca, st);
   }
   return adj ? launch_chain_cfg<TSmall, false, true>(ca, st) : launch_chain_cfg<TSmall, true, false>(ca, st);
 }
