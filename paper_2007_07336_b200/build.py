@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblmg.so")
 SOURCES = ["lmg.cu", "lmg_sweep.cu", "lmg_tgemm.cu"]
-DEPS = ["lmg_gemm.cuh", "lmg_conv.cuh", "lmg_sweep.cuh", "lmg_async.cuh", "lmg_tgemm.cuh"]
+DEPS = ["lmg_gemm.cuh", "lmg_conv.cuh", "lmg_sweep.cuh", "lmg_async.cuh", "lmg_tgemm.cuh", "lmg_chain.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -58,6 +58,21 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// spin until *f >= n: relaxed polls, then ONE acquire fence (an ld.acquire per poll invalidates
+// the SM's L1 every iteration -- ncu showed the CCTL.IVALL of the polls among the top stalls)
+__device__ __forceinline__ void wait_count(const unsigned* f, unsigned n) {
+  if (ld_relaxed(f) < n) {
+    do {
+      __nanosleep(32);
+    } while (ld_relaxed(f) < n);
+  }
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 
 template <class T, bool AK, bool BKM, bool ASC>
 __global__ void __launch_bounds__(T::WM* T::WN * 32)
@@ -111,16 +126,30 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
       if (st < KT) lb.load_next(smem + st * C::STAGE + C::B_OFF);
     // wait for this task's previous step (all its tiles), and for the WAR guard
     if (tid == 0) {
-      if (s > 0) {
-        const unsigned* f = ca.flags + (int64_t)(s - 1) * ca.max_tasks + t;
-        while (ld_acquire(f) < (unsigned)ca.tiles) __nanosleep(32);
-      }
-      if (ca.war_last && s == ca.nsteps - 1 && t + 1 < ca.st[0].ntasks) {
-        const unsigned* f = ca.flags + t + 1;  // step 0 of task t+1 has read its input row
-        while (ld_acquire(f) < (unsigned)ca.tiles) __nanosleep(32);
-      }
+      if (s > 0) wait_count(ca.flags + (int64_t)(s - 1) * ca.max_tasks + t, (unsigned)ca.tiles);
+      // WAR guard: step 0 of task t+1 has read its input row (the one this step overwrites)
+      if (ca.war_last && s == ca.nsteps - 1 && t + 1 < ca.st[0].ntasks)
+        wait_count(ca.flags + t + 1, (unsigned)ca.tiles);
     }
     __syncthreads();
+    // the epilogue's x (this tile's columns of the input row) and bias, fetched now so their
+    // latency hides under the mainloop instead of stalling the epilogue (ncu: the epilogue's
+    // dependent DADDs were ~10% of the stall samples)
+    const int mrow0 = m0 + wm0 + fr, ncol0 = n0 + wn0 + 2 * fk;
+    const double* bias = cs.bias ? cs.bias + t * a.bias_ts : nullptr;
+    double xv[C::MT][C::NTF][2], bv[C::NTF][2];
+#pragma unroll
+    for (int j = 0; j < C::NTF; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) bv[j][e] = bias ? bias[ncol0 + j * 8 + e] : 0.0;
+#pragma unroll
+    for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NTF; ++j) {
+        const double2 x2 = *reinterpret_cast<const double2*>(A + (int64_t)(mrow0 + i * 8) * a.ldc + ncol0 + j * 8);
+        xv[i][j][0] = x2.x;
+        xv[i][j][1] = x2.y;
+      }
 #pragma unroll
     for (int st = 0; st < STAGES - 1; ++st) {
       if (st < KT) {
@@ -173,17 +202,29 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     }
     cp_wait<0>();
 
-    EpiPtrs q;
-    q.bias = cs.bias ? cs.bias + t * a.bias_ts : nullptr;
-    q.X = A;
-    q.S = cs.s ? cs.s + t * a.s_ts : nullptr;
-    q.Y = q.P = nullptr;
-    q.O = cs.out + t * cs.out_ts;
-    q.O2 = cs.out2 ? cs.out2 + t * a.out2_ts : nullptr;
-    StepArgs ea = a;  // h2 varies per step
-    ea.h2 = cs.h2;
-    double rowsq[C::MT];
-    epilogue<E_PROP>(ea, q, acc, m0 + wm0 + fr, n0 + wn0 + 2 * fk, rowsq);
+    // E_PROP (lmg_gemm.cuh epilogue, same operations in the same order): out = s + (x + h*act(pre)),
+    // out2 = x + h2*act(pre).  Fully tiled: every (m, n) is in range.
+    {
+      const double* S = cs.s ? cs.s + t * a.s_ts : nullptr;
+      double* O = cs.out + t * cs.out_ts;
+      double* O2 = cs.out2 ? cs.out2 + t * a.out2_ts : nullptr;
+      const double h = a.h, h2 = cs.h2;
+#pragma unroll
+      for (int i = 0; i < C::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NTF; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int64_t idx = (int64_t)(mrow0 + i * 8) * a.ldc + ncol0 + j * 8 + e;
+            double pre = acc[i][j][e];
+            if (bias) pre = __dadd_rn(pre, bv[j][e]);
+            const double v = act_fwd(a.act, pre);
+            const double x = xv[i][j][e];
+            const double adv = __dadd_rn(x, __dmul_rn(h, v));
+            O[idx] = __dadd_rn(S ? S[idx] : 0.0, adv);
+            if (O2) O2[idx] = __dadd_rn(x, __dmul_rn(h2, v));
+          }
+    }
 
     __syncthreads();  // every thread's stores issued before the completion is published
     if (tid == 0) {

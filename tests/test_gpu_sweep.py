@@ -93,3 +93,22 @@ def test_tma_step_gemm_is_bitwise_the_default_routing(case, tmp_path):
         assert dflt["routes"][ROUTES.index("step_wide_full")] > 0
     for key in ("U0", "hist", "cyc", "U1", "lam", "loss", "adj_hist", "adj_cyc", "W", "b", "Us"):
         assert np.array_equal(tma[key], dflt[key], equal_nan=True), key
+
+
+@pytest.mark.parametrize("case", [(256, 512, 16, 16, 4), (128, 256, 16, 4, 8), (64, 128, 16, 4, 0, "relu")],
+                         ids=lambda c: "N%d_q%d_B%d_c%d" % c[:4] + "".join("_" + x for x in c[5:]))
+def test_chain_launch_is_bitwise_the_per_step_path(case, tmp_path):
+    """Persistent chain launches (one cooperative grid per FCF part, per-(step, block) completion
+    counters) against one launch per layer step: the same k-ascending DMMA chain and epilogue per
+    output, so the whole training step is bitwise -- for the default chain tile and the measured
+    alternatives (LMG_CHAIN_TILE)."""
+    from paper_2007_07336_b200._lib import ROUTES
+
+    base = {"LMG_NO_SWEEP": "1"}  # the fine and coarse levels on step launches / chains
+    per_step = _run(case, tmp_path, dict(base, LMG_NO_CHAIN="1"))
+    assert per_step["routes"][ROUTES.index("chain")] == 0
+    for tile in ("1", "0", "2", "5"):
+        ch = _run(case, tmp_path, dict(base, LMG_CHAIN_TILE=tile))
+        assert ch["routes"][ROUTES.index("chain")] > 0, tile
+        for key in ("U0", "hist", "cyc", "U1", "lam", "loss", "adj_hist", "adj_cyc", "W", "b", "Us"):
+            assert np.array_equal(ch[key], per_step[key], equal_nan=True), (tile, key)

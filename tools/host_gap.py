@@ -50,7 +50,8 @@ def main():
     X = torch.from_numpy(P.random_batch(q, [0, N, q], B)).to(dev)
     view = d._lmg_view()
     sizes = [N]
-    while sizes[-1] > cfg["threshold"]:
+    thr = cfg["threshold"] or N // c  # None: two levels (multigrid.py:76-102 default)
+    while sizes[-1] > thr:
         sizes.append(sizes[-1] // c)
     nlev = len(sizes)
     f0 = _dense_apply(d.Wo, d.bo, d.open_act, X).contiguous()

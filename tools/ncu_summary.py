@@ -1,6 +1,10 @@
 """Key metrics of ncu --set full reports -> JSON (profiles/).
 
-    python tools/ncu_summary.py out.json name=report.ncu-rep [...]"""
+    python tools/ncu_summary.py out.json name=report.ncu-rep [name=raw.csv ...]
+
+The first argument is the OUTPUT file.  Inputs are reports, or the `--page raw --csv` export of
+one (written on the GPU box, where the reports are too big to bring back).  Refuses to overwrite
+an input."""
 import csv
 import io
 import json
@@ -17,7 +21,11 @@ KEYS = ["Kernel Name", "Grid Size", "Block Size", "Cluster Size", "gpu__time_dur
 
 
 def summarize(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units, vals = rows[0], rows[1], rows[2]
     d = {}
@@ -37,6 +45,8 @@ def summarize(rep):
 
 
 if __name__ == "__main__":
+    if not sys.argv[1].endswith(".json") or "=" in sys.argv[1]:
+        sys.exit("usage: ncu_summary.py out.json name=report [...] (the first argument is the output)")
     res = {}
     for arg in sys.argv[2:]:
         name, rep = arg.split("=", 1)
