@@ -302,6 +302,9 @@ def load_traffic(config):
     try:
         with open(p) as fh:
             d = json.load(fh)
+        per = d.get("traffic_per_launch")  # round 2+: {config: dram bytes of one dominant launch}
+        if per is not None:
+            return per.get(config), d
         if d.get("config") != config:
             return None, d
         return d.get("dram_bytes_per_launch"), d

@@ -706,9 +706,8 @@ ConvGeom geom_of(const lmg_system& S) {
   return g;
 }
 
-template <int V>
-int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
-  using T = typename std::conditional<V == CV_ADJ, CTA, CT>::type;
+template <int V, class T>
+int launch_conv_t(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
   static_assert(T::BM == CT::BM && T::BN == CT::BN, "geometry padding assumes CT's tile");
   constexpr int A_SZ = T::BK * T::LDA;
   constexpr int B_SZ = (V == CV_ADJ) ? T::BN * T::LDB_K : T::BK * T::LDB_MN;
@@ -726,6 +725,37 @@ int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
                        (V == CV_PGRAD ? (double)(a.K / g.HWp) : (double)(a.M / g.HWp));
   route(V == CV_FWD ? LMG_ROUTE_CONV_FWD : V == CV_ADJ ? LMG_ROUTE_CONV_ADJ : LMG_ROUTE_CONV_PGRAD);
   return launch(cls, flops, 0.0, st, [&] { kern<<<grid, T::NT, SMEM, st>>>(a, g); });
+}
+
+// LMG_CONV_CFG=f,a,s (measurement knob): forward stages f in {2,3,4}, adjoint stages a in {2,3},
+// adjoint act' scaling once per staged element s in {0,1}; same tile shape (so the residual
+// partials, and every result, are bitwise the same)
+int conv_cfg(int i) {
+  static const int3 v = [] {
+    const char* e = getenv("LMG_CONV_CFG");
+    int f = 4, ad = 3, sc = 0;
+    if (e) sscanf(e, "%d,%d,%d", &f, &ad, &sc);
+    return make_int3(f, ad, sc);
+  }();
+  return i == 0 ? v.x : i == 1 ? v.y : v.z;
+}
+
+template <int V>
+int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
+  if (V == CV_FWD) {
+    const int f = conv_cfg(0);
+    if (f == 2) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 2>>(a, g, st);
+    if (f == 3) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 3>>(a, g, st);
+    return launch_conv_t<V, CT>(a, g, st);
+  }
+  if (V == CV_ADJ) {
+    const int ad = conv_cfg(1), sc = conv_cfg(2);
+    if (ad == 2 && sc) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 2, true>>(a, g, st);
+    if (ad == 2) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 2>>(a, g, st);
+    if (sc) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 3, true>>(a, g, st);
+    return launch_conv_t<V, CTA>(a, g, st);
+  }
+  return launch_conv_t<V, CT>(a, g, st);
 }
 
 // residual partial slots per state row (one per CTA tile of a row, canonical per tile config)

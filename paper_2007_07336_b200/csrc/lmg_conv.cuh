@@ -30,9 +30,12 @@ struct ConvGeom {
   int64_t q;
 };
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, bool SCALE_ONCE_ = false>
 struct ConvTile {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
+  // adjoint: act' applied once per staged element by the thread that copied it (as step_gemm's
+  // scale_own) instead of to every fragment at use
+  static constexpr bool SCALE_ONCE = SCALE_ONCE_;
   static constexpr int NT = WM * WN * 32;
   static constexpr int LDA = BM + 4;  // A tiles are stored [k][m] (m contiguous)
   static constexpr int LDB_MN = BN + 4;
@@ -228,6 +231,15 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
   const int fr = lane >> 2, fk = lane & 3;
   for (int kt = 0; kt < KT; ++kt) {
     cp_wait<STAGES - 2>();
+    if constexpr (V == CV_ADJ && T::SCALE_ONCE) {
+      // this thread's own elements of stage kt (conv_load_raster_idx's e -> (kk, mm) mapping)
+      double* as = smem + (kt % STAGES) * STAGE;
+#pragma unroll
+      for (int e = tid; e < BK * BM; e += T::NT) {
+        const int o = (e / BM) * T::LDA + e % BM;
+        as[o] = __dmul_rn(as[o], as[A_SZ + o]);
+      }
+    }
     __syncthreads();
     {
       const int nk = kt + STAGES - 1;
@@ -245,7 +257,7 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
       for (int i = 0; i < MT; ++i) {
         const int mm = wm0 + i * 8 + fr, k = kk + fk;
         af[i] = As[k * T::LDA + mm];
-        if (V == CV_ADJ) af[i] = __dmul_rn(af[i], Asc[k * T::LDA + mm]);
+        if (V == CV_ADJ && !T::SCALE_ONCE) af[i] = __dmul_rn(af[i], Asc[k * T::LDA + mm]);
       }
 #pragma unroll
       for (int j = 0; j < NTF; ++j) {

@@ -140,6 +140,11 @@ int main(int argc, char** argv) {
     run<Tile<32, 32, 16, 2, 2, 4>, false, true>(a, reps, "adj 32x32x16 2x2w 4st", ref.data(), tmp.data(), nout);
     run<Tile<32, 32, 16, 2, 2, 2>, false, true>(a, reps, "adj 32x32x16 2x2w 2st", ref.data(), tmp.data(), nout);
     run<TileR<32, 128, 16, 2, 4>, false, true>(a, reps, "adj RS 32x128x16 2x4w", ref.data(), tmp.data(), nout);
+    // residual-compatible (canonical partials: BN 32, two 16-column warps)
+    run<TileR<64, 32, 16, 2, 2>, false, true>(a, reps, "adj RS 64x32x16 2x2w", ref.data(), tmp.data(), nout);
+    run<TileR<64, 32, 16, 4, 2>, false, true>(a, reps, "adj RS 64x32x16 4x2w", ref.data(), tmp.data(), nout);
+    run<TileR<128, 32, 16, 4, 2>, false, true>(a, reps, "adj RS 128x32x16 4x2w", ref.data(), tmp.data(), nout);
+    run<TileR<128, 32, 16, 8, 2>, false, true>(a, reps, "adj RS 128x32x16 8x2w", ref.data(), tmp.data(), nout);
     run<TileR<32, 64, 16, 2, 4>, false, true>(a, reps, "adj RS 32x64x16 2x4w", ref.data(), tmp.data(), nout);
     run<TileR<32, 32, 16, 2, 2>, false, true>(a, reps, "adj RS 32x32x16 2x2w", ref.data(), tmp.data(), nout);
     run<TileR<64, 128, 16, 2, 4>, false, true>(a, reps, "adj RS 64x128x16 2x4w", ref.data(), tmp.data(), nout);
