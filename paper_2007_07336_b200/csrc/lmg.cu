@@ -481,11 +481,17 @@ using TTiny = Tile<16, 32, 16, 1, 2, 4>;   // batches <= 16: 2 warps of 16x16, n
 // (TileR: act' never enters shared memory) at 64x128 30.6 (64 tasks 25.2 -> 29.3); unscaled 30.5.
 using TFwd = Tile<32, 32, 16, 2, 2, 2>;
 using TAdj = TileR<64, 128, 16, 2, 4>;
+// adjoint residual steps (E_RESID: the canonical partials need 32-column tiles of two 16-column
+// warps): register-staged 64 x 32 tiles, 26.0 TF/s vs 22.4 for TFwd's 32 x 32 (4 tile shapes
+// measured, tools/tile_probe.cu); the partials are per row and tile, so bitwise the same
+using TResA = TileR<64, 32, 16, 2, 2>;
+using TTiny4 = Tile<16, 32, 16, 1, 4, 4>;  // batches <= 16, 4 warps of 16x8 (chain launches' tile)
 // parameter gradients of a small batch (K = B <= 32: one or two k-tiles): deeper rings only cost
 // occupancy (TWide's 4 stages left 3 CTAs/SM for a launch that streams W in and out)
 using TPg = Tile<32, 64, 16, 2, 4, 2>;
 static_assert(TTiny::BN == TSmall::BN && TTiny::WN == TSmall::WN, "canonical residual partials");
 static_assert(TFwd::BN == TSmall::BN && TFwd::WN == TSmall::WN, "canonical residual partials");
+static_assert(TResA::BN == TSmall::BN && TResA::WN == TSmall::WN, "canonical residual partials");
 
 template <class T, bool AK, bool BKM, bool ASC, int VEC, bool FULL = false>
 int launch_cfg(const StepArgs& a, cudaStream_t st) {
@@ -515,7 +521,8 @@ int launch_cfg(const StepArgs& a, cudaStream_t st) {
   static const bool pdl_multi = getenv("LMG_PDL_MULTI") != nullptr;
   const bool single = (int64_t)grid.x * grid.y * grid.z <= (int64_t)per_sm * num_sms();
   const bool pdl = pdl_on && (single || pdl_multi);
-  route(std::is_same<T, TTiny>::value ? (FULL ? LMG_ROUTE_STEP_TINY_FULL : LMG_ROUTE_STEP_TINY)
+  route((std::is_same<T, TTiny>::value || std::is_same<T, TTiny4>::value)
+            ? (FULL ? LMG_ROUTE_STEP_TINY_FULL : LMG_ROUTE_STEP_TINY)
         : (std::is_same<T, TWide>::value || std::is_same<T, TAdj>::value || std::is_same<T, TPg>::value)
             ? (FULL ? LMG_ROUTE_STEP_WIDE_FULL : LMG_ROUTE_STEP_WIDE)
                                         : (FULL ? LMG_ROUTE_STEP_SMALL_FULL : LMG_ROUTE_STEP_SMALL));
@@ -587,6 +594,10 @@ int launch_layout(const StepArgs& a, bool v2, cudaStream_t st) {
   };
   const int sel = choose_tile<AK, BKM, ASC>(a);
   if (sel == SEL_TINY) {
+    // non-residual small-batch steps on the chain launches' 4-warp 16 x 32 tile (residual steps
+    // keep TTiny's two 16-column warps: canonical partials)
+    if (a.epi != E_RESID && full(TTiny4::BM, TTiny4::BN, TTiny4::BK))
+      return launch_cfg<TTiny4, AK, BKM, ASC, 2, true>(a, st);
     if (full(TTiny::BM, TTiny::BN, TTiny::BK)) return launch_cfg<TTiny, AK, BKM, ASC, 2, true>(a, st);
     return launch_cfg<TTiny, AK, BKM, ASC, 2>(a, st);
   }
@@ -596,6 +607,8 @@ int launch_layout(const StepArgs& a, bool v2, cudaStream_t st) {
     if (full(TWide::BM, TWide::BN, TWide::BK)) return launch_cfg<TWide, AK, BKM, ASC, 2, true>(a, st);
     return launch_cfg<TWide, AK, BKM, ASC, 2>(a, st);
   }
+  if (AK && !BKM && ASC && full(TResA::BM, TResA::BN, TResA::BK))
+    return launch_cfg<TResA, AK, BKM, ASC, 2, true>(a, st);
   if (full(TFwd::BM, TFwd::BN, TFwd::BK)) return launch_cfg<TFwd, AK, BKM, ASC, 2, true>(a, st);
   return launch_cfg<TSmall, AK, BKM, ASC, 2>(a, st);
 }
@@ -711,7 +724,7 @@ int launch_conv_t(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
   static_assert(T::BM == CT::BM && T::BN == CT::BN, "geometry padding assumes CT's tile");
   constexpr int A_SZ = T::BK * T::LDA;
   constexpr int B_SZ = (V == CV_ADJ) ? T::BN * T::LDB_K : T::BK * T::LDB_MN;
-  constexpr int STAGE = A_SZ * (V == CV_ADJ ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
+  constexpr int STAGE = A_SZ * ((V == CV_ADJ && !T::RS) ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
   constexpr size_t SMEM = (size_t)T::STAGES * STAGE * sizeof(double);
   auto kern = conv_gemm<T, V>;
   static const cudaError_t attr =
@@ -728,8 +741,8 @@ int launch_conv_t(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
 }
 
 // LMG_CONV_CFG=f,a,s (measurement knob): forward stages f in {2,3,4}, adjoint stages a in {2,3},
-// adjoint act' scaling once per staged element s in {0,1}; same tile shape (so the residual
-// partials, and every result, are bitwise the same)
+// adjoint act' scaling s: 0 per fragment, 1 once per staged element, 2 register-staged (2 stages);
+// same tile shape (so the residual partials, and every result, are bitwise the same)
 int conv_cfg(int i) {
   static const int3 v = [] {
     const char* e = getenv("LMG_CONV_CFG");
@@ -750,6 +763,7 @@ int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
   }
   if (V == CV_ADJ) {
     const int ad = conv_cfg(1), sc = conv_cfg(2);
+    if (sc == 2) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 2, false, true>>(a, g, st);
     if (ad == 2 && sc) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 2, true>>(a, g, st);
     if (ad == 2) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 2>>(a, g, st);
     if (sc) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 3, true>>(a, g, st);

@@ -30,12 +30,17 @@ struct ConvGeom {
   int64_t q;
 };
 
-template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, bool SCALE_ONCE_ = false>
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, bool SCALE_ONCE_ = false,
+          bool RS_ = false>
 struct ConvTile {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
   // adjoint: act' applied once per staged element by the thread that copied it (as step_gemm's
   // scale_own) instead of to every fragment at use
   static constexpr bool SCALE_ONCE = SCALE_ONCE_;
+  // adjoint, register-staged (as step_gemm's TileR): each thread gathers its lambda and act'
+  // elements of the NEXT k-tile into registers while this k-tile's DMMAs run and stores their
+  // product into the A stage (act' never enters shared memory; 2 stages)
+  static constexpr bool RS = RS_;
   static constexpr int NT = WM * WN * 32;
   static constexpr int LDA = BM + 4;  // A tiles are stored [k][m] (m contiguous)
   static constexpr int LDB_MN = BN + 4;
@@ -122,7 +127,9 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
   // [BN][BK+4] (ADJ, K-major); PGRAD's B also needs a scale tile
   constexpr int A_SZ = BK * T::LDA;
   constexpr int B_SZ = (V == CV_ADJ) ? BN * T::LDB_K : BK * T::LDB_MN;
-  constexpr int STAGE = A_SZ * (V == CV_ADJ ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
+  constexpr bool RS = (V == CV_ADJ) && T::RS;
+  static_assert(!RS || STAGES == 2, "register staging: 2 stages");
+  constexpr int STAGE = A_SZ * ((V == CV_ADJ && !RS) ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
   extern __shared__ __align__(16) double smem[];
   __shared__ double red[T::NT / 32];
 
@@ -155,12 +162,14 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
       const int dy = tap / 3, dx = tap % 3;
       const int sy = (V == CV_FWD) ? dy - 1 : 1 - dy, sx = (V == CV_FWD) ? dx - 1 : 1 - dx;
       if (V == CV_ADJ) {
-        conv_load_raster_idx<T>(base, A, g, b0, p0, ch0, sy, sx, tid);
-        conv_load_raster_idx<T>(base + A_SZ, Ds, g, b0, p0, ch0, sy, sx, tid);
+        if (!RS) {  // RS: the A stage is written from registers (rs_gather / rs_store)
+          conv_load_raster_idx<T>(base, A, g, b0, p0, ch0, sy, sx, tid);
+          conv_load_raster_idx<T>(base + A_SZ, Ds, g, b0, p0, ch0, sy, sx, tid);
+        }
       } else {
         conv_load_raster<T>(base, A, g, b0, rpix, ch0, sy, sx, tid);
       }
-      double* bs = base + A_SZ * (V == CV_ADJ ? 2 : 1);
+      double* bs = base + A_SZ * ((V == CV_ADJ && !RS) ? 2 : 1);
       // weight rows are contiguous: 16-byte vectors when C is even (pairs never straddle the
       // channel bound and stay 16B-aligned); the padded smem rows keep 16B alignment
       const bool vec = (g.C & 1) == 0 && (reinterpret_cast<uintptr_t>(Bm) & 15) == 0;
@@ -222,10 +231,47 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
     }
   };
 
+  // register-staged adjoint A: this thread's elements e = tid + i*NT of a k-tile
+  constexpr int EPT = (BK * BM + T::NT - 1) / T::NT;
+  double ra[RS ? EPT : 1], rd[RS ? EPT : 1];
+  auto rs_gather = [&](int kt) {
+    const int k0 = kt * BK;
+    const int tap = k0 / g.Cp, ch0 = k0 % g.Cp;
+    const int sy = 1 - tap / 3, sx = 1 - tap % 3;
+    const double* xb = A + (int64_t)b0 * g.q;
+    const double* db = Ds + (int64_t)b0 * g.q;
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_stage(s, s);
+    for (int i = 0; i < EPT; ++i) {
+      const int e = tid + i * T::NT;
+      const int kk = e / BM, mm = e % BM;
+      const int pix = p0 + mm;
+      const int yy = pix / g.W + sy, xx = pix % g.W + sx;
+      const bool ok = e < BK * BM && (pix < g.HW) && (ch0 + kk < g.C) && (yy >= 0) && (yy < g.H) &&
+                      (xx >= 0) && (xx < g.W);
+      const int64_t o = (int64_t)(ch0 + kk) * g.HW + yy * g.W + xx;
+      ra[i] = ok ? xb[o] : 0.0;
+      rd[i] = ok ? db[o] : 0.0;
+    }
+  };
+  auto rs_store = [&](double* as) {
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = tid + i * T::NT;
+      if (e < BK * BM) as[(e / BM) * T::LDA + e % BM] = __dmul_rn(ra[i], rd[i]);
+    }
+  };
+  if constexpr (RS) {
+    rs_gather(0);
+    rs_store(smem);
+    load_stage(0, 0);  // the weight tile of k-tile 0
     cp_commit();
+    if (KT > 1) rs_gather(1);
+  } else {
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (s < KT) load_stage(s, s);
+      cp_commit();
+    }
   }
   const int wm0 = wm * WTM, wn0 = wn * WTN;
   const int fr = lane >> 2, fk = lane & 3;
@@ -248,7 +294,7 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
     }
     const double* As = smem + (kt % STAGES) * STAGE;
     const double* Asc = As + A_SZ;
-    const double* Bs = As + A_SZ * (V == CV_ADJ ? 2 : 1);
+    const double* Bs = As + A_SZ * ((V == CV_ADJ && !RS) ? 2 : 1);
     const double* Bsc = Bs + B_SZ;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
@@ -257,7 +303,7 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
       for (int i = 0; i < MT; ++i) {
         const int mm = wm0 + i * 8 + fr, k = kk + fk;
         af[i] = As[k * T::LDA + mm];
-        if (V == CV_ADJ && !T::SCALE_ONCE) af[i] = __dmul_rn(af[i], Asc[k * T::LDA + mm]);
+        if (V == CV_ADJ && !T::SCALE_ONCE && !RS) af[i] = __dmul_rn(af[i], Asc[k * T::LDA + mm]);
       }
 #pragma unroll
       for (int j = 0; j < NTF; ++j) {
@@ -273,6 +319,12 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
       for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int j = 0; j < NTF; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    if constexpr (RS) {
+      if (kt + 1 < KT) {  // stage kt+1's buffer was last read in iteration kt-1 (barrier passed)
+        rs_store(smem + ((kt + 1) % STAGES) * STAGE);
+        if (kt + 2 < KT) rs_gather(kt + 2);
+      }
     }
   }
   cp_wait<0>();
