@@ -1031,7 +1031,10 @@ int chain_steps(const lmg_system& S, int B, const Fam* fams, int nsteps, bool wa
       default: return go(Tile<16, 32, 16, 1, 4, 4>{});
     }
   }
-  return adj ? launch_chain_cfg<TSmall, false, true>(ca, st) : launch_chain_cfg<TSmall, true, false>(ca, st);
+  // batches > 16 (opt-in, LMG_CHAIN_ALL=1): forward sweeps on TFwd; the adjoint keeps its
+  // register-staged 64 x 128 step launches
+  if (adj) return -1;
+  return launch_chain_cfg<TFwd, true, false>(ca, st);
 }
 
 int family(const lmg_system& S, int B, int epi, const Fam& f, cudaStream_t st) {

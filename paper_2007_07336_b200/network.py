@@ -33,15 +33,20 @@ class DeviceStack:
         self.geometry = geometry  # (channels, height, width) for conv2d
 
     @classmethod
-    def from_blocks(cls, blocks):
+    def from_blocks(cls, blocks, W_host=None, b_host=None):
+        """Upload the blocks.  W_host / b_host: the already stacked host copy (e.g. a pinned
+        mirror) to upload from instead of stacking the block arrays again."""
         t = require_cuda()
         first = blocks[0]
         acts = {blk.activation for blk in blocks}
         kinds = {blk.kind for blk in blocks}
         if len(acts) != 1 or len(kinds) != 1:
             raise ConfigurationError("the device path needs one activation and kind for all blocks")
-        W = t.from_numpy(np.stack([np.asarray(blk.weights, dtype=np.float64) for blk in blocks])).cuda()
-        b = t.from_numpy(np.stack([np.asarray(blk.bias, dtype=np.float64) for blk in blocks])).cuda()
+        if W_host is None:
+            W_host = t.from_numpy(np.stack([np.asarray(blk.weights, dtype=np.float64) for blk in blocks]))
+            b_host = t.from_numpy(np.stack([np.asarray(blk.bias, dtype=np.float64) for blk in blocks]))
+        W = W_host.cuda()
+        b = b_host.cuda()
         geom = None
         if first.kind == "conv2d":
             geom = (first.weights.shape[3], first.height, first.width)
@@ -149,6 +154,7 @@ class ResidualNetwork:
                 f"readout expects width {self.readout.input_width}, network width is {q}")
         self._device = None
         self._host_ref, self._block_ids = [], []
+        self._mirror = None
 
     @property
     def num_blocks(self) -> int:
@@ -159,44 +165,56 @@ class ResidualNetwork:
         return self.blocks[0].input_width
 
     # -- device mirror ------------------------------------------------------------------
+    # The device stack is paired with a pinned host mirror: the host image of the device
+    # parameters at the last synchronisation.  It is the upload source, the D2H target of
+    # pull_from_device(), and the reference the host arrays are compared with (views, no copy of
+    # its own): a train_epoch over a 2 GiB network moves theta over PCIe once each way per epoch
+    # from pinned memory, with one host copy into the block arrays (tools/train_epoch_bench.py).
     def device_stack(self) -> DeviceStack:
         """The device copy of the block parameters, kept in sync with the host arrays.
 
         The reference edits parameters in place and never rebuilds anything (multigrid.py:83-85,
         training.py:231; its finite-difference tests perturb ``flat[i]`` and re-evaluate), so
-        every use compares the host arrays with the copy taken at the last upload and re-uploads
-        exactly the blocks that changed (or rebuilds when the block list changed).  Device-side
-        training updates the stack in place; `pull_from_device()` copies it back to the host
-        arrays (and re-bases the comparison copy)."""
+        every use compares the host arrays with the mirror taken at the last synchronisation and
+        re-uploads exactly the blocks that changed (or rebuilds when the block list changed).
+        Device-side training updates the stack in place; `pull_from_device()` copies it back to
+        the host arrays (through the mirror)."""
         blocks = self.blocks
         if self._device is None or len(self._host_ref) != len(blocks) or any(
                 a is not blk for a, blk in zip(self._block_ids, blocks)):
-            self._device = DeviceStack.from_blocks(blocks)
-            self._snapshot()
-            return self._device
+            return self._rebuild()
         stale = [i for i, blk in enumerate(blocks)
                  if not (np.array_equal(blk.weights, self._host_ref[i][0])
                          and np.array_equal(blk.bias, self._host_ref[i][1]))]
         if stale:
-            t = require_cuda()
             if any(np.shape(blocks[i].weights) != self._host_ref[i][0].shape for i in stale):
-                self._device = DeviceStack.from_blocks(blocks)
-                self._snapshot()
-                return self._device
-            idx = t.tensor(stale, device=self._device.W.device)
-            W = np.stack([np.asarray(blocks[i].weights, dtype=np.float64) for i in stale])
-            b = np.stack([np.asarray(blocks[i].bias, dtype=np.float64) for i in stale])
-            self._device.W.index_copy_(0, idx, t.from_numpy(W).to(self._device.W.device))
-            self._device.b.index_copy_(0, idx, t.from_numpy(b).to(self._device.b.device))
-            for i in stale:
-                self._host_ref[i] = (np.array(blocks[i].weights, dtype=np.float64, copy=True),
-                                     np.array(blocks[i].bias, dtype=np.float64, copy=True))
+                return self._rebuild()
+            mW, mb = self._mirror
+            for i in stale:  # the mirror rows (and so _host_ref) follow, then those rows upload
+                mW.numpy()[i] = blocks[i].weights
+                mb.numpy()[i] = blocks[i].bias
+                self._device.W[i].copy_(mW[i])
+                self._device.b[i].copy_(mb[i])
         return self._device
 
-    def _snapshot(self):
-        self._block_ids = list(self.blocks)
-        self._host_ref = [(np.array(blk.weights, dtype=np.float64, copy=True),
-                           np.array(blk.bias, dtype=np.float64, copy=True)) for blk in self.blocks]
+    def _rebuild(self) -> DeviceStack:
+        t = require_cuda()
+        blocks = self.blocks
+        wshape = (len(blocks),) + tuple(np.shape(blocks[0].weights))
+        bshape = (len(blocks),) + tuple(np.shape(blocks[0].bias))
+        mW = t.empty(wshape, dtype=t.float64, pin_memory=True)
+        mb = t.empty(bshape, dtype=t.float64, pin_memory=True)
+        nW, nb = mW.numpy(), mb.numpy()
+        for i, blk in enumerate(blocks):
+            if np.shape(blk.weights) != wshape[1:] or np.shape(blk.bias) != bshape[1:]:
+                raise ConfigurationError("the device path needs blocks of one shape")
+            nW[i] = blk.weights
+            nb[i] = blk.bias
+        self._mirror = (mW, mb)
+        self._device = DeviceStack.from_blocks(blocks, mW, mb)
+        self._block_ids = list(blocks)
+        self._host_ref = [(nW[i], nb[i]) for i in range(len(blocks))]
+        return self._device
 
     def invalidate_device(self):
         self._device = None
@@ -204,12 +222,13 @@ class ResidualNetwork:
     def pull_from_device(self):
         if self._device is None:
             return
-        W = self._device.W.cpu().numpy()
-        b = self._device.b.cpu().numpy()
+        mW, mb = self._mirror
+        mW.copy_(self._device.W)  # device -> pinned mirror
+        mb.copy_(self._device.b)
+        nW, nb = mW.numpy(), mb.numpy()
         for i, blk in enumerate(self.blocks):
-            blk.weights[...] = W[i]
-            blk.bias[...] = b[i]
-        self._snapshot()
+            blk.weights[...] = nW[i]
+            blk.bias[...] = nb[i]
 
     def _lmg_view(self) -> SystemView:
         return SystemView(self.device_stack(), 1, self.step_size, self.num_blocks)

@@ -288,12 +288,21 @@ def train_epoch(net: ResidualNetwork, data: Dataset, cfg: TrainConfig, rng=None,
     dev = dnet.Wo.device
     losses, hits = [], t.zeros((), dtype=t.int64, device=dev)
     images = data.images.reshape(len(data), -1)
+    # per batch size: states, act', adjoint and the two source heads at stable addresses, so every
+    # batch's solves replay the library's cached cycle graphs (new tensors per batch meant a graph
+    # capture per solve) and no (N, B, q) stack is reallocated
+    bufs = {}
     for lo in range(0, len(order), cfg.batch_size):
         batch = order[lo : lo + cfg.batch_size]
         X = t.from_numpy(np.ascontiguousarray(images[batch], dtype=np.float64)).to(dev)
         labels = t.from_numpy(np.asarray(data.labels[batch], dtype=np.int64)).to(dev)
-        f0 = _dense_apply(dnet.Wo, dnet.bo, dnet.open_act, X)
-        U = t.empty((view.n,) + tuple(f0.shape), dtype=t.float64, device=dev)
+        Bb = len(batch)
+        if Bb not in bufs:
+            shape = (view.n, Bb, view.width)
+            bufs[Bb] = tuple(t.empty(shape, dtype=t.float64, device=dev) for _ in range(3)) + tuple(
+                t.empty((Bb, view.width), dtype=t.float64, device=dev) for _ in range(2))
+        U, D_buf, lam_buf, f0, head = bufs[Bb]
+        f0.copy_(_dense_apply(dnet.Wo, dnet.bo, dnet.open_act, X))
         if cfg.mode == "exact":
             _lib.call("lmg_sequential_forward", view.desc(), U.shape[1], f0.data_ptr(), _lib.SRC_HEAD,
                       U.data_ptr(), _lib.stream_handle())
@@ -302,7 +311,8 @@ def train_epoch(net: ResidualNetwork, data: Dataset, cfg: TrainConfig, rng=None,
                          src_mode=_lib.SRC_HEAD, use_initial=False, tol=cfg.solve_tol,
                          max_cycles=cfg.mg_cycles)
         r = backward(dnet, U, X, labels, adjoint="sequential", scale=1.0 / len(batch),
-                     lr=float(cfg.learning_rate), want_grads=False)
+                     lr=float(cfg.learning_rate), want_grads=False, lam_buf=lam_buf, D_buf=D_buf,
+                     head_buf=head)
         losses.append(r.loss)
         hits += (r.logits.argmax(dim=1) == labels).sum()
     _write_back(net, dnet)
