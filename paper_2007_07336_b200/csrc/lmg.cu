@@ -724,7 +724,7 @@ int launch_conv_t(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
   static_assert(T::BM == CT::BM && T::BN == CT::BN, "geometry padding assumes CT's tile");
   constexpr int A_SZ = T::BK * T::LDA;
   constexpr int B_SZ = (V == CV_ADJ) ? T::BN * T::LDB_K : T::BK * T::LDB_MN;
-  constexpr int STAGE = A_SZ * ((V == CV_ADJ && !T::RS) ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
+  constexpr int STAGE = A_SZ * ((V == CV_ADJ && !T::RS && !T::PRE) ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
   constexpr size_t SMEM = (size_t)T::STAGES * STAGE * sizeof(double);
   auto kern = conv_gemm<T, V>;
   static const cudaError_t attr =
@@ -764,6 +764,9 @@ int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
   if (V == CV_ADJ) {
     const int ad = conv_cfg(1), sc = conv_cfg(2);
     if (sc == 2) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 2, false, true>>(a, g, st);
+    // 9: the pre-scaled kernel alone on the UNSCALED operand (wrong results: a speed bound only)
+    if (sc == 9) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 3, false, false, true>>(a, g, st);
+    if (sc == 8) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 4, false, false, true>>(a, g, st);
     if (ad == 2 && sc) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 2, true>>(a, g, st);
     if (ad == 2) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 2>>(a, g, st);
     if (sc) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 3, true>>(a, g, st);

@@ -31,8 +31,11 @@ struct ConvGeom {
 };
 
 template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_, bool SCALE_ONCE_ = false,
-          bool RS_ = false>
+          bool RS_ = false, bool PRE_ = false>
 struct ConvTile {
+  // adjoint with a pre-scaled A operand (lambda * act' computed by a separate pass): one raster
+  // tile per stage, no scaling in the kernel
+  static constexpr bool PRE = PRE_;
   static constexpr int BM = BM_, BN = BN_, BK = BK_, WM = WM_, WN = WN_, STAGES = STAGES_;
   // adjoint: act' applied once per staged element by the thread that copied it (as step_gemm's
   // scale_own) instead of to every fragment at use
@@ -128,8 +131,9 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
   constexpr int A_SZ = BK * T::LDA;
   constexpr int B_SZ = (V == CV_ADJ) ? BN * T::LDB_K : BK * T::LDB_MN;
   constexpr bool RS = (V == CV_ADJ) && T::RS;
+  constexpr bool PRE = (V == CV_ADJ) && T::PRE;
   static_assert(!RS || STAGES == 2, "register staging: 2 stages");
-  constexpr int STAGE = A_SZ * ((V == CV_ADJ && !RS) ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
+  constexpr int STAGE = A_SZ * ((V == CV_ADJ && !RS && !PRE) ? 2 : 1) + B_SZ * (V == CV_PGRAD ? 2 : 1);
   extern __shared__ __align__(16) double smem[];
   __shared__ double red[T::NT / 32];
 
@@ -162,14 +166,16 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
       const int dy = tap / 3, dx = tap % 3;
       const int sy = (V == CV_FWD) ? dy - 1 : 1 - dy, sx = (V == CV_FWD) ? dx - 1 : 1 - dx;
       if (V == CV_ADJ) {
-        if (!RS) {  // RS: the A stage is written from registers (rs_gather / rs_store)
+        if (PRE) {  // A is lambda * act' already
+          conv_load_raster_idx<T>(base, A, g, b0, p0, ch0, sy, sx, tid);
+        } else if (!RS) {  // RS: the A stage is written from registers (rs_gather / rs_store)
           conv_load_raster_idx<T>(base, A, g, b0, p0, ch0, sy, sx, tid);
           conv_load_raster_idx<T>(base + A_SZ, Ds, g, b0, p0, ch0, sy, sx, tid);
         }
       } else {
         conv_load_raster<T>(base, A, g, b0, rpix, ch0, sy, sx, tid);
       }
-      double* bs = base + A_SZ * ((V == CV_ADJ && !RS) ? 2 : 1);
+      double* bs = base + A_SZ * ((V == CV_ADJ && !RS && !PRE) ? 2 : 1);
       // weight rows are contiguous: 16-byte vectors when C is even (pairs never straddle the
       // channel bound and stay 16B-aligned); the padded smem rows keep 16B alignment
       const bool vec = (g.C & 1) == 0 && (reinterpret_cast<uintptr_t>(Bm) & 15) == 0;
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
     }
     const double* As = smem + (kt % STAGES) * STAGE;
     const double* Asc = As + A_SZ;
-    const double* Bs = As + A_SZ * ((V == CV_ADJ && !RS) ? 2 : 1);
+    const double* Bs = As + A_SZ * ((V == CV_ADJ && !RS && !PRE) ? 2 : 1);
     const double* Bsc = Bs + B_SZ;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
@@ -303,7 +309,7 @@ __global__ void __launch_bounds__(T::NT) conv_gemm(const StepArgs a, const ConvG
       for (int i = 0; i < MT; ++i) {
         const int mm = wm0 + i * 8 + fr, k = kk + fk;
         af[i] = As[k * T::LDA + mm];
-        if (V == CV_ADJ && !T::SCALE_ONCE && !RS) af[i] = __dmul_rn(af[i], Asc[k * T::LDA + mm]);
+        if (V == CV_ADJ && !T::SCALE_ONCE && !RS && !PRE) af[i] = __dmul_rn(af[i], Asc[k * T::LDA + mm]);
       }
 #pragma unroll
       for (int j = 0; j < NTF; ++j) {
