@@ -77,6 +77,23 @@ __global__ void k_copy_rows(double* __restrict__ dst, int64_t dst_ts, const doub
   }
 }
 
+// out[t][e] = a[t][e] * d[t][e] for the rows of every task (the conv adjoint's lambda * act'
+// operand, computed once instead of per gathered raster tile); len even, 16-byte aligned rows
+__global__ void k_prescale(double* __restrict__ out, const double* __restrict__ a, int64_t a_ts,
+                           const double* __restrict__ d, int64_t d_ts, int64_t ntasks, int64_t len) {
+  const int64_t half = len / 2, total = ntasks * half;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / half, i = 2 * (e - t * half);
+    const double2 x = *reinterpret_cast<const double2*>(a + t * a_ts + i);
+    const double2 y = *reinterpret_cast<const double2*>(d + t * d_ts + i);
+    double2 r;
+    r.x = __dmul_rn(x.x, y.x);
+    r.y = __dmul_rn(x.y, y.y);
+    *reinterpret_cast<double2*>(out + t * len + i) = r;
+  }
+}
+
 // multigrid.py:227  states[::c] += solved - coarse_states   (coarse_states == states[::c] bitwise)
 __global__ void k_correct(double* __restrict__ U, int64_t u_ts, const double* __restrict__ V,
                           int64_t v_ts, int64_t nrows, int64_t len) {
@@ -753,6 +770,40 @@ int conv_cfg(int i) {
   return i == 0 ? v.x : i == 1 ? v.y : v.z;
 }
 
+// per-(device, stream) device scratch, grown outside stream capture only (nullptr when a capture
+// would need a new or bigger buffer: callers fall back to a path without it)
+double* stream_scratch(cudaStream_t st, size_t bytes) {
+  struct Buf { int dev; cudaStream_t st; double* p; size_t n; };
+  static std::mutex mu;
+  static std::vector<Buf> bufs;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  Buf* b = nullptr;
+  for (auto& x : bufs)
+    if (x.dev == dev && x.st == st) b = &x;
+  if (b && b->n >= bytes) return b->p;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs != cudaStreamCaptureStatusNone) return nullptr;
+  if (b) {
+    cudaStreamSynchronize(st);  // the old buffer may still be in use by this stream
+    cudaFree(b->p);
+    b->p = nullptr;
+    b->n = 0;
+  } else {
+    bufs.push_back(Buf{dev, st, nullptr, 0});
+    b = &bufs.back();
+  }
+  if (cudaMalloc(&b->p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    b->p = nullptr;
+    return nullptr;
+  }
+  b->n = bytes;
+  return b->p;
+}
+
 template <int V>
 int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
   if (V == CV_FWD) {
@@ -763,6 +814,28 @@ int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
   }
   if (V == CV_ADJ) {
     const int ad = conv_cfg(1), sc = conv_cfg(2);
+    // default: lambda * act' computed once per element by k_prescale into a stream scratch, then
+    // the adjoint conv stages one raster tile per k-step (c3 launch: 1.91 ms with the scaling in
+    // the kernel -- two gathered raster tiles per stage -- vs 1.62 + 0.13 ms; tools/conv_probe.py).
+    // Same __dmul_rn products: bitwise.
+    static const bool no_pre = getenv("LMG_CONV_NO_PRESCALE") != nullptr;
+    if (sc == 0 && !no_pre) {
+      const int64_t len = (int64_t)(a.M / g.HWp) * g.q;  // B samples x q per task
+      const bool ok = (len % 2 == 0) && (a.A_ts % 2 == 0) && (a.Ds_ts % 2 == 0) &&
+                      aligned16(a.A) && aligned16(a.Ds);
+      double* scr = ok ? stream_scratch(st, (size_t)a.ntasks * len * sizeof(double)) : nullptr;
+      if (scr) {
+        TRY(launch(CLS_ELEM, 0.0, 24.0 * a.ntasks * len, st, [&] {
+          k_prescale<<<grid_for(a.ntasks * len / 2), 256, 0, st>>>(scr, a.A, a.A_ts, a.Ds, a.Ds_ts,
+                                                                    a.ntasks, len);
+        }));
+        StepArgs p = a;
+        p.A = scr;
+        p.A_ts = len;
+        p.Ds = nullptr;
+        return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 3, false, false, true>>(p, g, st);
+      }
+    }
     if (sc == 2) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 2, false, true>>(a, g, st);
     // 9: the pre-scaled kernel alone on the UNSCALED operand (wrong results: a speed bound only)
     if (sc == 9) return launch_conv_t<V, ConvTile<32, 64, 16, 2, 2, 3, false, false, true>>(a, g, st);
