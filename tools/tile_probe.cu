@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../paper_2007_07336_b200/csrc/lmg_gemm.cuh"
+#include "gemmx_experiment.cuh"
 
 using namespace lmg;
 
@@ -66,6 +67,47 @@ float run(const StepArgs& a, int reps, const char* name, const double* ref, doub
   return best;
 }
 
+template <bool DB>
+float run_x(const StepArgs& a, int reps, const char* name, const double* ref, double* out_host, size_t nout) {
+  using X = TileX;
+  auto kern = step_gemm_x<DB>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)X::SMEM));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, X::NT, X::SMEM));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  dim3 grid(a.N / X::BN, a.M / X::BM, a.ntasks);
+  StepArgs al = a;
+  al.pdl_late = 1;
+  kern<<<grid, X::NT, X::SMEM>>>(al);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t s, e;
+  cudaEventCreate(&s);
+  cudaEventCreate(&e);
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(s);
+    kern<<<grid, X::NT, X::SMEM>>>(al);
+    cudaEventRecord(e);
+    CK(cudaEventSynchronize(e));
+    float ms;
+    cudaEventElapsedTime(&ms, s, e);
+    if (ms < best) best = ms;
+  }
+  const double flops = 2.0 * a.ntasks * (double)a.M * a.N * a.K;
+  bool same = true;
+  if (ref) {
+    CK(cudaMemcpy(out_host, a.out, nout * 8, cudaMemcpyDeviceToHost));
+    same = !memcmp(out_host, ref, nout * 8);
+  }
+  const double waves = (double)grid.x * grid.y * grid.z / (per_sm * 148.0);
+  printf("%-34s %6.3f ms %6.2f TF/s  regs %3d  smem %6zu  CTAs/SM %d  waves %5.2f  %s (spill-local %zu)\n", name, best,
+         flops / (best * 1e-3) / 1e12, fa.numRegs, X::SMEM, per_sm, waves,
+         ref ? (same ? "bitwise" : "DIFFERS") : "(reference)", fa.localSizeBytes);
+  return best;
+}
+
 int main(int argc, char** argv) {
   const int tasks = argc > 1 ? atoi(argv[1]) : 256;
   const int M = argc > 2 ? atoi(argv[2]) : 256;
@@ -106,6 +148,18 @@ int main(int argc, char** argv) {
   const int reps = 10;
   const int group = argc > 5 ? atoi(argv[5]) : 0;
   printf("tasks %d  M %d  N %d  K %d  group %d\n", tasks, M, N, K, group);
+  if (group == 3) {  // big-warp-tile kernel vs the production forward tile
+    run<Tile<32, 32, 16, 2, 2, 2>>(a, reps, "TFwd 32x32x16 2st (production)", nullptr, nullptr, 0);
+    CK(cudaMemcpy(ref.data(), out, nout * 8, cudaMemcpyDeviceToHost));
+    run_x<true>(a, reps, "X 64x128 4w 32x64 3st DB", ref.data(), tmp.data(), nout);
+    run_x<false>(a, reps, "X 64x128 4w 32x64 3st", ref.data(), tmp.data(), nout);
+    a.act = LMG_ACT_IDENTITY;
+    run<Tile<32, 32, 16, 2, 2, 2>>(a, reps, "identity TFwd", nullptr, nullptr, 0);
+    CK(cudaMemcpy(ref.data(), out, nout * 8, cudaMemcpyDeviceToHost));
+    run_x<true>(a, reps, "identity X 64x128 DB", ref.data(), tmp.data(), nout);
+    run_x<false>(a, reps, "identity X 64x128", ref.data(), tmp.data(), nout);
+    a.act = LMG_ACT_TANH;
+  }
   if (group == 0 || group == 1) {  // forward layout, E_PROP tanh
     run<Tile<32, 32, 16, 2, 2, 4>>(a, reps, "32x32x16 2x2w 4st (production)", nullptr, nullptr, 0);
     CK(cudaMemcpy(ref.data(), out, nout * 8, cudaMemcpyDeviceToHost));
