@@ -1,7 +1,7 @@
 // Step-GEMM tile-shape probe on the c2 forward layer step (256 tasks x B 256 x q 512, E_PROP
 // tanh epilogue): TF/s per tile configuration of lmg::step_gemm and a bitwise check against the
 // production 32x32 tile (every configuration runs the same k-ascending DMMA chain per output).
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude \
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude -I<venv>/flashinfer/data/cutlass/include \
 //        -o /tmp/tile_probe tools/tile_probe.cu && /tmp/tile_probe [tasks] [M] [N] [K]
 #include <cstdio>
 #include <cstdlib>
@@ -10,6 +10,7 @@
 
 #include "../paper_2007_07336_b200/csrc/lmg_gemm.cuh"
 #include "gemmx_experiment.cuh"
+#include "cutlass_experiment.cuh"
 
 using namespace lmg;
 
@@ -108,6 +109,46 @@ float run_x(const StepArgs& a, int reps, const char* name, const double* ref, do
   return best;
 }
 
+float run_c(const StepArgs& a, int reps, const char* name, const double* ref, double* out_host, size_t nout) {
+  using CF = CutlassFwd;
+  auto kern = step_gemm_cutlass;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, CF::NT, CF::SMEM));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, kern));
+  dim3 grid(a.N / CF::BN, a.M / CF::BM, a.ntasks);
+  StepArgs al = a;
+  al.pdl_late = 1;
+  kern<<<grid, CF::NT, CF::SMEM>>>(al);
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t s, e;
+  cudaEventCreate(&s);
+  cudaEventCreate(&e);
+  float best = 1e30f;
+  for (int r = 0; r < reps; ++r) {
+    cudaEventRecord(s);
+    kern<<<grid, CF::NT, CF::SMEM>>>(al);
+    cudaEventRecord(e);
+    CK(cudaEventSynchronize(e));
+    float ms;
+    cudaEventElapsedTime(&ms, s, e);
+    if (ms < best) best = ms;
+  }
+  const double flops = 2.0 * a.ntasks * (double)a.M * a.N * a.K;
+  bool same = true;
+  if (ref) {
+    CK(cudaMemcpy(out_host, a.out, nout * 8, cudaMemcpyDeviceToHost));
+    same = !memcmp(out_host, ref, nout * 8);
+  }
+  const double waves = (double)grid.x * grid.y * grid.z / (per_sm * 148.0);
+  printf("%-34s %6.3f ms %6.2f TF/s  regs %3d  smem %6zu  CTAs/SM %d  waves %5.2f  %s (spill-local %zu)\n", name, best,
+         flops / (best * 1e-3) / 1e12, fa.numRegs, CF::SMEM, per_sm, waves,
+         ref ? (same ? "bitwise" : "DIFFERS") : "(reference)", fa.localSizeBytes);
+  return best;
+}
+
 int main(int argc, char** argv) {
   const int tasks = argc > 1 ? atoi(argv[1]) : 256;
   const int M = argc > 2 ? atoi(argv[2]) : 256;
@@ -151,11 +192,13 @@ int main(int argc, char** argv) {
   if (group == 3) {  // big-warp-tile kernel vs the production forward tile
     run<Tile<32, 32, 16, 2, 2, 2>>(a, reps, "TFwd 32x32x16 2st (production)", nullptr, nullptr, 0);
     CK(cudaMemcpy(ref.data(), out, nout * 8, cudaMemcpyDeviceToHost));
+    run_c(a, reps, "CUTLASS mainloop 64x128 + staged epi", ref.data(), tmp.data(), nout);
     run_x<true>(a, reps, "X 64x128 4w 32x64 3st DB", ref.data(), tmp.data(), nout);
     run_x<false>(a, reps, "X 64x128 4w 32x64 3st", ref.data(), tmp.data(), nout);
     a.act = LMG_ACT_IDENTITY;
     run<Tile<32, 32, 16, 2, 2, 2>>(a, reps, "identity TFwd", nullptr, nullptr, 0);
     CK(cudaMemcpy(ref.data(), out, nout * 8, cudaMemcpyDeviceToHost));
+    run_c(a, reps, "identity CUTLASS mainloop", ref.data(), tmp.data(), nout);
     run_x<true>(a, reps, "identity X 64x128 DB", ref.data(), tmp.data(), nout);
     run_x<false>(a, reps, "identity X 64x128", ref.data(), tmp.data(), nout);
     a.act = LMG_ACT_TANH;
