@@ -675,6 +675,11 @@ int launch_serial(Layout L, const StepArgs& a, cudaStream_t st) {
   const int64_t base = (int64_t)(a.N / BN) * (a.M / BM);
   int KS = 1;
   while (KS < 8 && base * KS * 2 <= 4 * num_sms() && (a.K / BK) % (KS * 2) == 0) KS *= 2;
+  static const int ks_force = [] {  // LMG_SPLITK_KS (measurement knob): 2, 4 or 8
+    const char* e = getenv("LMG_SPLITK_KS");
+    return e ? atoi(e) : 0;
+  }();
+  if (ks_force >= 2 && ks_force <= 8 && (a.K / BK) % ks_force == 0) KS = ks_force;
   if (KS == 1) return -1;
   const bool adj = (L == L_ADJ);
   if (tiny)

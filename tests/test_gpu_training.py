@@ -50,39 +50,45 @@ def test_finite_difference_gradients():
             assert abs(fd - grad[idx]) <= 1e-5 * max(1e-3, abs(fd)), (idx, fd, grad[idx])
 
 
-def test_train_epoch_matches_oracle():
+@pytest.mark.parametrize("n,epochs", [(12, 1), (10, 2)])
+def test_train_epoch_matches_oracle(n, epochs):
+    """(10, 2): a ragged last batch (4, 4, 2) and a second epoch on the same network -- the per-
+    batch-size device buffers and the pinned parameter mirror carried across epochs."""
     rng = np.random.default_rng(3)
-    n = 12
     images = rng.random((n, 28, 28))
     labels = rng.integers(0, 10, n)
     data = P.Dataset(images, labels)
     net = P.random_network(16, 8, [3, 16, 8], input_dim=784, horizon=1.0)
     a = fas.random_network_arrays(16, 8, [3, 16, 8], input_dim=784, horizon=1.0)
     cfg = P.TrainConfig(learning_rate=0.1, batch_size=4, epochs=1, mg_cycles=2)
-    stats = P.train_epoch(net, data, cfg, rng=np.random.default_rng(7))
+    train_rng = np.random.default_rng(7)
+    for _ in range(epochs):
+        stats = P.train_epoch(net, data, cfg, rng=train_rng)
     # oracle: training.py:255-289 with oracle/fas.py pieces
-    order = np.random.default_rng(7).permutation(n)
+    oracle_rng = np.random.default_rng(7)
     W, b, Wo, bo, Wr, br = (a["W"].copy(), a["b"].copy(), a["Wo"].copy(), a["bo"].copy(),
                             a["Wr"].copy(), a["br"].copy())
-    losses = []
-    for lo in range(0, n, 4):
-        idx = order[lo : lo + 4]
-        X = images[idx].reshape(len(idx), -1)
-        onet = fas.Net(Wo, bo, "tanh", fas.DenseLevel(W, b, "tanh", a["step"]), Wr, br, "identity")
-        src = onet.source(X)
-        U, _, _ = fas.solve(fas.build_levels(onet.blocks, 4), 4, src, 1e-12, 2)
-        final, logits = fas.adjoint_head(onet, U)
-        loss, dl = fas.loss_and_dlogits(logits, labels[idx])
-        losses += list(loss)
-        gfin, gpr = fas.g_final_from(onet, final, dl)
-        D = fas.derivs(onet.blocks, U)
-        mu, lam0 = fas.adjoint_sequential(fas.adjoint_level(onet.blocks, D), gfin)
-        gW, gb = fas.block_grads(onet.blocks, U, mu, D, 1.0 / len(idx))
-        gpo = lam0 * fas.act_deriv("tanh", X @ Wo.T + bo)
-        gWo, gbo = gpo.T @ X / len(idx), gpo.sum(0) / len(idx)
-        gWr, gbr = gpr.T @ final / len(idx), gpr.sum(0) / len(idx)
-        W, b = W - 0.1 * gW, b - 0.1 * gb
-        Wo, bo, Wr, br = Wo - 0.1 * gWo, bo - 0.1 * gbo, Wr - 0.1 * gWr, br - 0.1 * gbr
+    for _ in range(epochs):
+        order = oracle_rng.permutation(n)
+        losses = []
+        for lo in range(0, n, 4):
+            idx = order[lo : lo + 4]
+            X = images[idx].reshape(len(idx), -1)
+            onet = fas.Net(Wo, bo, "tanh", fas.DenseLevel(W, b, "tanh", a["step"]), Wr, br, "identity")
+            src = onet.source(X)
+            U, _, _ = fas.solve(fas.build_levels(onet.blocks, 4), 4, src, 1e-12, 2)
+            final, logits = fas.adjoint_head(onet, U)
+            loss, dl = fas.loss_and_dlogits(logits, labels[idx])
+            losses += list(loss)
+            gfin, gpr = fas.g_final_from(onet, final, dl)
+            D = fas.derivs(onet.blocks, U)
+            mu, lam0 = fas.adjoint_sequential(fas.adjoint_level(onet.blocks, D), gfin)
+            gW, gb = fas.block_grads(onet.blocks, U, mu, D, 1.0 / len(idx))
+            gpo = lam0 * fas.act_deriv("tanh", X @ Wo.T + bo)
+            gWo, gbo = gpo.T @ X / len(idx), gpo.sum(0) / len(idx)
+            gWr, gbr = gpr.T @ final / len(idx), gpr.sum(0) / len(idx)
+            W, b = W - 0.1 * gW, b - 0.1 * gb
+            Wo, bo, Wr, br = Wo - 0.1 * gWo, bo - 0.1 * gbo, Wr - 0.1 * gWr, br - 0.1 * gbr
     got = np.stack([blk.weights for blk in net.blocks])
     assert np.max(np.abs(got - W)) <= 1e-11
     assert np.max(np.abs(net.opening.weights - Wo)) <= 1e-11
