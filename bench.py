@@ -50,6 +50,12 @@ CONFIGS = {
     "c5": dict(depth=1024, width=512, batch=16, cf=16, threshold=4, tol=1e-9, max_cycles=50, lr=0.1,
                workload="dense tanh ResNet 1024 layers width 512 batch 16, 3-level FAS cf 16 "
                         "forward+adjoint training step to tol 1e-9"),
+    # BASELINE.json configs[4]'s shortest-critical-path point at the reference's survey shape
+    # (q 16, one sample, cf 16, levels [1024, 64, 4]): the latency-bound regime,
+    # where the FAS step beats layer-by-layer GPU propagation already on one GPU
+    "c6": dict(depth=1024, width=16, batch=1, cf=16, threshold=4, tol=1e-9, max_cycles=50, lr=0.1,
+               workload="dense tanh ResNet 1024 layers width 16 batch 1, 3-level FAS cf 16 "
+                        "(levels [1024,64,4]) forward+adjoint training step to tol 1e-9"),
 }
 
 METRIC = "FAS fwd+adjoint solve time to tol; layer*samples/s"
@@ -564,8 +570,10 @@ def run_ours(args, cfg):
                       frac=achieved / pk if pk else None,
                       traffic=traffic,
                       kernel="relaxation/residual layer-step class, FP64 DMMA m8n8k4 with fused FAS "
-                             "epilogues: lmg::step_gemm (forward steps) + lmg::tgemm_kernel "
-                             "(warp-specialised TMA, adjoint steps); conv configs: lmg::conv_gemm",
+                             "epilogues: lmg::step_gemm (forward: 2-stage 32x32 tiles; adjoint: "
+                             "register-staged act'-scaled 64x128 / 64x32 tiles; batches <= 16: "
+                             "16-row tiles) + lmg::chain_gemm (persistent chain launches of "
+                             "small-batch sweeps); conv configs: lmg::conv_gemm",
                       peak_source=pk_src,
                       algorithmic=alg,
                       intensity_flop_per_byte=intensity, fp64_ridge_flop_per_byte=ridge,
