@@ -1110,7 +1110,8 @@ int chain_steps(const lmg_system& S, int B, const Fam* fams, int nsteps, bool wa
       case 6: return go(Tile<16, 128, 16, 1, 8, 4>{});
       case 7: return go(Tile<16, 32, 16, 1, 4, 5>{});
       case 8: return go(Tile<16, 64, 16, 1, 8, 3>{});
-      default: return go(Tile<16, 32, 16, 1, 4, 4>{});
+      default:  // (the adjoint at 3 stages -- 7 CTAs/SM instead of 5 -- measured the same)
+        return go(Tile<16, 32, 16, 1, 4, 4>{});
     }
   }
   // batches > 16 (opt-in, LMG_CHAIN_ALL=1): forward sweeps on TFwd; the adjoint keeps its
