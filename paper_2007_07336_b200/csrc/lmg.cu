@@ -1110,7 +1110,11 @@ int chain_steps(const lmg_system& S, int B, const Fam* fams, int nsteps, bool wa
       case 6: return go(Tile<16, 128, 16, 1, 8, 4>{});
       case 7: return go(Tile<16, 32, 16, 1, 4, 5>{});
       case 8: return go(Tile<16, 64, 16, 1, 8, 3>{});
-      default:  // (the adjoint at 3 stages -- 7 CTAs/SM instead of 5 -- measured the same)
+      case 9: return go(Tile<16, 32, 16, 1, 4, 4>{});  // the adjoint with act' staged in smem
+      default:
+        // (the adjoint at 3 stages -- 7 CTAs/SM instead of 5 -- measured the same as 4; the
+        // register-staged act' keeps 4 stages at 7 CTAs/SM)
+        if (adj) return go(TileRW<16, 32, 16, 1, 4, 4>{});
         return go(Tile<16, 32, 16, 1, 4, 4>{});
     }
   }

@@ -150,18 +150,50 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
         xv[i][j][0] = x2.x;
         xv[i][j][1] = x2.y;
       }
+    // register-staged act' scaling (C::RS, the adjoint): each thread's lambda and act' vectors of
+    // the next k-tile are loaded into registers during this k-tile's DMMAs and their product is
+    // stored into the next stage's A area -- act' never occupies shared memory (the staged act'
+    // tile had cost the adjoint chain 2 of the forward's 7 CTAs per SM)
+    constexpr int RIT = decltype(la)::IT;
+    double2 ra[C::RS ? RIT : 1], rd[C::RS ? RIT : 1];
+    auto rs_ldg = [&] {
 #pragma unroll
-    for (int st = 0; st < STAGES - 1; ++st) {
-      if (st < KT) {
-        double* base = smem + st * C::STAGE;
-        la.load_next(base);
-        if (ASC) ld_.load_next(base + C::A_SZ);
+      for (int i = 0; i < RIT; ++i) {
+        if (RIT * C::NTHREADS > decltype(la)::NV && la.tid_out_of_range(i)) continue;
+        ra[i] = *reinterpret_cast<const double2*>(la.cur[i]);
+        rd[i] = *reinterpret_cast<const double2*>(ld_.cur[i]);
+        la.cur[i] += la.kadv;
+        ld_.cur[i] += ld_.kadv;
       }
-      cp_commit();  // group 0 also carries the prefetched weight stages
+    };
+    auto rs_sts = [&](double* base) {
+#pragma unroll
+      for (int i = 0; i < RIT; ++i) {
+        if (RIT * C::NTHREADS > decltype(la)::NV && la.tid_out_of_range(i)) continue;
+        *reinterpret_cast<double2*>(base + la.soff[i]) =
+            make_double2(__dmul_rn(ra[i].x, rd[i].x), __dmul_rn(ra[i].y, rd[i].y));
+      }
+    };
+    if constexpr (C::RS) {
+      rs_ldg();
+      rs_sts(smem);  // A of stage 0
+#pragma unroll
+      for (int st = 0; st < STAGES - 1; ++st) cp_commit();  // the prefetched weight stages
+      if (KT > 1) rs_ldg();
+    } else {
+#pragma unroll
+      for (int st = 0; st < STAGES - 1; ++st) {
+        if (st < KT) {
+          double* base = smem + st * C::STAGE;
+          la.load_next(base);
+          if (ASC) ld_.load_next(base + C::A_SZ);
+        }
+        cp_commit();  // group 0 also carries the prefetched weight stages
+      }
     }
     for (int kt = 0; kt < KT; ++kt) {
       cp_wait<STAGES - 2>();
-      if (ASC) {
+      if (ASC && !C::RS) {
         double* st0 = smem + (kt % STAGES) * C::STAGE;
         la.scale_own(st0, st0 + C::A_SZ);
       }
@@ -170,8 +202,10 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
         const int nk = kt + STAGES - 1;
         if (nk < KT) {
           double* base = smem + (nk % STAGES) * C::STAGE;
-          la.load_next(base);
-          if (ASC) ld_.load_next(base + C::A_SZ);
+          if (!C::RS) {
+            la.load_next(base);
+            if (ASC) ld_.load_next(base + C::A_SZ);
+          }
           lb.load_next(base + C::B_OFF);
         }
         cp_commit();
@@ -198,6 +232,14 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
         for (int i = 0; i < C::MT; ++i)
 #pragma unroll
           for (int j = 0; j < C::NTF; ++j) dmma(acc[i][j][0], acc[i][j][1], af[cur][i], bf[cur][j]);
+      }
+      if constexpr (C::RS) {
+        // stage kt+1's A area was last read at k-tile kt+1-STAGES (every warp passed this
+        // k-tile's barrier since); it is published by the next k-tile's barrier
+        if (kt + 1 < KT) {
+          rs_sts(smem + ((kt + 1) % STAGES) * C::STAGE);
+          if (kt + 2 < KT) rs_ldg();
+        }
       }
     }
     cp_wait<0>();

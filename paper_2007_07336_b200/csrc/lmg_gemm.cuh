@@ -357,6 +357,12 @@ template <int BM_, int BN_, int BK_, int WM_, int WN_>
 struct TileR : Tile<BM_, BN_, BK_, WM_, WN_, 2> {
   static constexpr bool RS = true;
 };
+// the same staging with a deeper weight ring (persistent chain launches: the W stages run ahead
+// of each item's dependency wait; A goes through registers one k-tile ahead)
+template <int BM_, int BN_, int BK_, int WM_, int WN_, int STAGES_>
+struct TileRW : Tile<BM_, BN_, BK_, WM_, WN_, STAGES_> {
+  static constexpr bool RS = true;
+};
 
 template <class T, bool AK, bool BKM, bool ASC>
 struct GemmCfg {

@@ -107,7 +107,7 @@ def test_chain_launch_is_bitwise_the_per_step_path(case, tmp_path):
     base = {"LMG_NO_SWEEP": "1"}  # the fine and coarse levels on step launches / chains
     per_step = _run(case, tmp_path, dict(base, LMG_NO_CHAIN="1"))
     assert per_step["routes"][ROUTES.index("chain")] == 0
-    for tile in ("1", "0", "2", "5"):
+    for tile in ("1", "0", "2", "5", "9"):
         ch = _run(case, tmp_path, dict(base, LMG_CHAIN_TILE=tile))
         assert ch["routes"][ROUTES.index("chain")] > 0, tile
         for key in ("U0", "hist", "cyc", "U1", "lam", "loss", "adj_hist", "adj_cyc", "W", "b", "Us"):
