@@ -692,8 +692,9 @@ __global__ void __launch_bounds__(T::WM* T::WN * 32)
     case E_COARSE_R: epilogue<E_COARSE_R>(a, q, acc, mrow0, ncol0, rowsq); break;
     case E_PROPOP: epilogue<E_PROPOP>(a, q, acc, mrow0, ncol0, rowsq); break;
     case E_DERIV: epilogue<E_DERIV>(a, q, acc, mrow0, ncol0, rowsq); break;
-    case E_PGRAD:  // only the parameter-gradient layout (A MN-major) runs it (loads of W before
-      // the mainloop instead measured slower: 1.23 vs 1.07 ms per c5 gradient launch)
+    case E_PGRAD:  // only the parameter-gradient layout (A MN-major) runs it (measured and not
+      // kept: W loaded into registers before the mainloop, 1.23 vs 1.07 ms per c5 gradient
+      // launch; W staged into shared memory by cp.async with the first stages, no change)
       if constexpr (!AK) epilogue<E_PGRAD>(a, q, acc, mrow0, ncol0, rowsq);
       break;
     case E_APPLY: epilogue<E_APPLY>(a, q, acc, mrow0, ncol0, rowsq); break;
