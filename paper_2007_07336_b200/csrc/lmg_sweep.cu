@@ -394,6 +394,10 @@ using Cfg32A = SwCfg<32, 2, 7, true>;
 // needs the 4-CTA clusters to stay in one wave
 using Cfg128F = SwCfg<128, 1, 5, false, 16>;
 using Cfg128A = SwCfg<128, 1, 4, true, 16>;
+// 16 columns per CTA, 16-k stages: narrow networks (q = 16 -- BASELINE.md 3.4's survey shape, the
+// latency-bound regime), one CTA per chain
+using Cfg16F = SwCfg<16, 1, 6, false, 16>;
+using Cfg16A = SwCfg<16, 1, 6, true, 16>;
 
 // run f with the configuration tag of (cfg, adjoint)
 template <class F>
@@ -401,6 +405,7 @@ auto with_cfg(int cfg, bool adj, F&& f) {
   switch (cfg) {
     case 0: return adj ? f(Cfg64A{}) : f(Cfg64F{});
     case 1: return adj ? f(Cfg32A{}) : f(Cfg32F{});
+    case 3: return adj ? f(Cfg16A{}) : f(Cfg16F{});
     default: return adj ? f(Cfg128A{}) : f(Cfg128F{});
   }
 }
@@ -504,6 +509,8 @@ int sweep_config(int q, int B, int adj, int nchains) {
   if (forced == 1 && ok32) return 1;
   if (forced == 2 && (adj ? fits<Cfg128A>(q) : fits<Cfg128F>(q))) return 2;
   if (nchains > 16 && ok64) return 0;
+  if (!ok32 && !ok64)  // q not a multiple of 32: the 16-column shape
+    return (adj ? fits<Cfg16A>(q) : fits<Cfg16F>(q)) ? 3 : -1;
   return ok32 ? 1 : (ok64 ? 0 : -1);
 }
 

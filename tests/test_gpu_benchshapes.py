@@ -47,7 +47,7 @@ CASES = {  # name: (N, q, B, c, threshold, max_cycles, kernel variants that must
     "c2_depth64": (64, 512, 256, 4, 4, 50, ("step_small_full", "step_wide_full", "serial_splitk")),
     "c4_depth32": (32, 1024, 128, 4, 8, 50, ("step_small_full", "step_wide_full")),
     # bench c6: BASELINE configs[4]'s shortest-critical-path point (q 16, one sample, cf 16)
-    "c6_full": (1024, 16, 1, 16, 4, 50, ("step_tiny",)),
+    "c6_full": (1024, 16, 1, 16, 4, 50, ("sweep_fcf", "sweep_seq")),
     # bench c1: the reference demo's shape
     "c1_full": (64, 32, 64, 4, 16, 50, ()),
 }

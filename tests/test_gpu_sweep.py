@@ -31,6 +31,8 @@ CASES = [
     (64, 512, 256, 4, 16),   # 16 batch tiles: serial solves on 4-CTA clusters (128 columns)
     (128, 128, 12, 4, 8, "relu"),      # the other fused activations
     (64, 256, 16, 4, 0, "identity"),
+    (64, 16, 4, 4, 0),       # 16-column shape (q = 16): one CTA per chain
+    (256, 16, 1, 16, 4),     # c6-shaped: q 16, one sample, cf 16, levels [256, 16, 1]
 ]
 
 
