@@ -154,7 +154,7 @@ def launch_count() -> int:
 
 ROUTES = ("step_small", "step_small_full", "step_wide", "step_wide_full", "step_tiny",
           "step_tiny_full", "tgemm_big", "tgemm_small", "serial_splitk", "sweep_fcf", "sweep_seq",
-          "conv_fwd", "conv_adj", "conv_pgrad", "chain")
+          "conv_fwd", "conv_adj", "conv_pgrad", "chain", "wsweep")
 
 
 def set_canonical_order(on: bool) -> bool:

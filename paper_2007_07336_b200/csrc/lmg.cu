@@ -66,9 +66,21 @@ inline cudaStream_t S_(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // ------------------------------------------------------------------------------------------
 // elementwise kernels (HBM-bound; grid-stride, 2 doubles per thread-iteration where possible)
+//
+// Programmatic dependent launch: each elementwise kernel waits for its upstream grid first and
+// then lets its own dependents launch, so in the latency-bound regime (a cycle of ~a dozen tiny
+// launches, c1 / c6) the next launch overlaps this one instead of following its drain.  Waiting
+// before triggering keeps the chain transitive: a dependent's pre-wait prologue (the step
+// kernels' W prefetch) only ever overlaps a kernel whose own upstream work is complete.
+// griddepcontrol.wait is a no-op for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __global__ void k_copy_rows(double* __restrict__ dst, int64_t dst_ts, const double* __restrict__ src,
                             int64_t src_ts, int64_t nrows, int64_t len) {
+  pdl_enter();
   const int64_t total = nrows * len;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -81,6 +93,7 @@ __global__ void k_copy_rows(double* __restrict__ dst, int64_t dst_ts, const doub
 // operand, computed once instead of per gathered raster tile); len even, 16-byte aligned rows
 __global__ void k_prescale(double* __restrict__ out, const double* __restrict__ a, int64_t a_ts,
                            const double* __restrict__ d, int64_t d_ts, int64_t ntasks, int64_t len) {
+  pdl_enter();
   const int64_t half = len / 2, total = ntasks * half;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -97,6 +110,7 @@ __global__ void k_prescale(double* __restrict__ out, const double* __restrict__ 
 // multigrid.py:227  states[::c] += solved - coarse_states   (coarse_states == states[::c] bitwise)
 __global__ void k_correct(double* __restrict__ U, int64_t u_ts, const double* __restrict__ V,
                           int64_t v_ts, int64_t nrows, int64_t len) {
+  pdl_enter();
   const int64_t total = nrows * len;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -108,6 +122,7 @@ __global__ void k_correct(double* __restrict__ U, int64_t u_ts, const double* __
 
 __global__ void k_add(double* __restrict__ out, const double* __restrict__ a,
                       const double* __restrict__ b, int64_t len) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = __dadd_rn(a[i], b[i]);
@@ -117,6 +132,7 @@ __global__ void k_add(double* __restrict__ out, const double* __restrict__ a,
 // residual row 0, multigrid.py:124,142); optionally V[0] = U[0] (the copy the recursion edits)
 __global__ void k_row0_coarse(const double* __restrict__ U0, const double* __restrict__ S0,
                               double* __restrict__ SH0, double* __restrict__ V0, int64_t len) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
        i += (int64_t)gridDim.x * blockDim.x) {
     double u = U0[i];
@@ -129,6 +145,7 @@ __global__ void k_row0_coarse(const double* __restrict__ U0, const double* __res
 __global__ void k_resid_row0(const double* __restrict__ S0, const double* __restrict__ U0,
                              double* __restrict__ R0, double* __restrict__ part, int64_t slot,
                              int B, int q) {
+  pdl_enter();
   __shared__ double sh[256];
   const int b = blockIdx.x;
   double acc = 0.0;
@@ -156,6 +173,7 @@ __global__ void k_resid_row0(const double* __restrict__ S0, const double* __rest
 // bit).  Dense systems (the partitioned path is dense-only).  One thread per sample.
 __global__ void k_resid_row0_tiles(const double* __restrict__ S0, const double* __restrict__ U0,
                                    double* __restrict__ part, int B, int q) {
+  pdl_enter();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   const double* s = S0 + (int64_t)b * q;
@@ -187,6 +205,7 @@ __global__ void k_resid_row0_tiles(const double* __restrict__ S0, const double* 
 // norms[b] = sqrt(sum over slots, in slot order) -- deterministic for any launch geometry
 __global__ void k_reduce_norms(const double* __restrict__ part, int64_t nslots, int B,
                                double* __restrict__ norms) {
+  pdl_enter();
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   double s = 0.0;
@@ -219,6 +238,7 @@ __global__ void k_bias_grads(const double* __restrict__ lam_top, int64_t lam_ts,
 // rank's own source row (network.py:100 `source[j] + (u + h*fv)`).
 __global__ void k_halo_finish(const double* __restrict__ s0, const double* __restrict__ adv,
                               double* __restrict__ out, int64_t len) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = __dadd_rn(s0 ? s0[i] : 0.0, adv[i]);
@@ -249,6 +269,7 @@ __global__ void k_cycle_book(const double* __restrict__ norms, int B, double tol
 // after a fused FCF sweep: U[0] = f[0] (c_relaxation, multigrid.py:157) and U[kc] = Cn[k], k >= 1
 __global__ void k_fcf_commit(double* __restrict__ U, const double* __restrict__ src0,
                              const double* __restrict__ Cn, int nb, int c, int64_t BQ) {
+  pdl_enter();
   const int64_t total = (int64_t)nb * BQ;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -264,6 +285,7 @@ __global__ void k_coarse_from_adv(const double* __restrict__ Uc, int64_t u_ts,
                                   const double* __restrict__ adv, const double* __restrict__ P,
                                   double* __restrict__ SH, double* __restrict__ V, int64_t nrows,
                                   int64_t len) {
+  pdl_enter();
   const int64_t total = nrows * len;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -279,6 +301,7 @@ __global__ void k_coarse_from_adv(const double* __restrict__ Uc, int64_t u_ts,
 __global__ void k_row0_coarse_halo(const double* __restrict__ U0, const double* __restrict__ adv,
                                    const double* __restrict__ P0, double* __restrict__ SH0,
                                    double* __restrict__ V0, int64_t len) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
        i += (int64_t)gridDim.x * blockDim.x) {
     double u = U0[i];
@@ -293,6 +316,7 @@ __global__ void k_row0_coarse_halo(const double* __restrict__ U0, const double* 
 __global__ void k_cpart(const double* __restrict__ U, const double* __restrict__ P,
                         const double* __restrict__ S0, int is_first, int c, int B, int q,
                         double* __restrict__ cpart) {
+  pdl_enter();
   __shared__ double sh[256];
   const int k = blockIdx.y, b = blockIdx.x;
   const int64_t BQ = (int64_t)B * q;
@@ -316,6 +340,7 @@ __global__ void k_cpart(const double* __restrict__ U, const double* __restrict__
 // block partials after the correction: block_part[k][b] = cpart[k][b] + sum_t fpart[k][t][b]
 __global__ void k_combine_post(const double* __restrict__ cpart, const double* __restrict__ fpart,
                                int nb, int nt, int B, double* __restrict__ block_part) {
+  pdl_enter();
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)nb * B) return;
   int k = (int)(e / B), b = (int)(e - (int64_t)k * B);
@@ -328,6 +353,7 @@ __global__ void k_combine_post(const double* __restrict__ cpart, const double* _
 // of its tile partials; row 0 of the rank comes from r0part
 __global__ void k_combine_full(const double* __restrict__ rpart, const double* __restrict__ r0part,
                                int nb, int c, int nt, int B, double* __restrict__ block_part) {
+  pdl_enter();
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= (int64_t)nb * B) return;
   int k = (int)(e / B), b = (int)(e - (int64_t)k * B);
@@ -396,6 +422,25 @@ int num_sms() {
 int grid_for(int64_t total) {
   int64_t g = (total + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)num_sms() * 16));
+}
+
+// launch of an elementwise kernel (one that starts with pdl_enter): with the programmatic
+// stream-serialization attribute when its grid fits one wave (multi-wave grids keep plain
+// launches, as the step kernels do).  LMG_NO_PDL=1 disables.
+template <class... KA, class... A>
+void ew_launch(void (*kern)(KA...), dim3 grid, int block, cudaStream_t st, A... args) {
+  static const bool pdl_on = getenv("LMG_NO_PDL") == nullptr && getenv("LMG_NO_PDL_ELEM") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  const int64_t blocks = (int64_t)grid.x * grid.y * grid.z;
+  cfg.numAttrs = (pdl_on && blocks <= (int64_t)num_sms() * (2048 / block)) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KA>(args)...);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -470,7 +515,7 @@ int copy_rows(double* dst, int64_t dst_ts, const double* src, int64_t src_ts, in
               int64_t len, cudaStream_t st) {
   if (nrows <= 0 || len <= 0) return LMG_OK;
   return launch(CLS_ELEM, 0.0, 16.0 * nrows * len, st, [&] {
-    k_copy_rows<<<grid_for(nrows * len), 256, 0, st>>>(dst, dst_ts, src, src_ts, nrows, len);
+    ew_launch(k_copy_rows, dim3(grid_for(nrows * len)), 256, st, dst, dst_ts, src, src_ts, nrows, len);
   });
 }
 
@@ -832,7 +877,7 @@ int launch_conv(const StepArgs& a, const ConvGeom& g, cudaStream_t st) {
       double* scr = ok ? stream_scratch(st, (size_t)a.ntasks * len * sizeof(double)) : nullptr;
       if (scr) {
         TRY(launch(CLS_ELEM, 0.0, 24.0 * a.ntasks * len, st, [&] {
-          k_prescale<<<grid_for(a.ntasks * len / 2), 256, 0, st>>>(scr, a.A, a.A_ts, a.Ds, a.Ds_ts,
+          ew_launch(k_prescale, dim3(grid_for(a.ntasks * len / 2)), 256, st, scr, a.A, a.A_ts, a.Ds, a.Ds_ts,
                                                                     a.ntasks, len);
         }));
         StepArgs p = a;
@@ -1276,6 +1321,7 @@ int run_sweep(const SweepArgs& a, const SweepShape& sh, double steps, double wri
   if (a.adj) bytes += steps * row;
   cudaError_t e = cudaSuccess;
   route(a.mode == SW_SEQ ? LMG_ROUTE_SWEEP_SEQ : LMG_ROUTE_SWEEP_FCF);
+  if (sh.cfg == SWEEP_CFG_WARP) route(LMG_ROUTE_WSWEEP);
   TRY(launch(a.adj ? CLS_SWEEP_ADJ : CLS_SWEEP_FWD, flops, bytes, st, [&] { e = sweep_launch(a, sh, st); }));
   if (e != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("sweep launch: ") + cudaGetErrorString(e));
   return LMG_OK;
@@ -1337,7 +1383,7 @@ int fcf_sweep(const lmg_system& S, int B, int c, double* U, const double* src, i
   TRY(run_sweep(a, sh, steps, written, st));
   const int64_t BQ = (int64_t)B * S.width;
   return launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
-    k_fcf_commit<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, src, Cn, nb, c, BQ);
+    ew_launch(k_fcf_commit, dim3(grid_for((int64_t)nb * BQ)), 256, st, U, src, Cn, nb, c, BQ);
   });
 }
 
@@ -1408,7 +1454,7 @@ int local_fcf_fused(const lmg_system& S, int B, int c, double* U, const double* 
   }
   if (part == 0 && nb > 0) {  // U[0] = f[0] on the first rank; U[kc] = Cn[k], k = 1..nb-1
     TRY(launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
-      k_fcf_commit<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, is_first ? src : nullptr, Cn, nb, c, BQ);
+      ew_launch(k_fcf_commit, dim3(grid_for((int64_t)nb * BQ)), 256, st, U, is_first ? src : nullptr, Cn, nb, c, BQ);
     }));
   }
   if (part == 1 && has_next && adv_out && advH)
@@ -1616,15 +1662,15 @@ int local_coarse_source(const lmg_system& S, int B, int c, const double* U, cons
   if (advH) {  // S_H[n] = (U[nc] - advH[n-1]) + (P[n] - U[nc]); V[n] = U[nc]: elementwise
     if (nb > 1)
       TRY(launch(CLS_ELEM, 0.0, 40.0 * (nb - 1) * BQ, st, [&] {
-        k_coarse_from_adv<<<grid_for((int64_t)(nb - 1) * BQ), 256, 0, st>>>(
+        ew_launch(k_coarse_from_adv, dim3(grid_for((int64_t)(nb - 1) * BQ)), 256, st, 
             U + (int64_t)c * BQ, c * BQ, advH, P + BQ, SH + BQ, V ? V + BQ : nullptr, nb - 1, BQ);
       }));
     if (is_first)
       return launch(CLS_ELEM, 0.0, 24.0 * BQ, st, [&] {
-        k_row0_coarse<<<grid_for(BQ), 256, 0, st>>>(U, src, SH, V, BQ);
+        ew_launch(k_row0_coarse, dim3(grid_for(BQ)), 256, st, U, src, SH, V, BQ);
       });
     return launch(CLS_ELEM, 0.0, 32.0 * BQ, st, [&] {
-      k_row0_coarse_halo<<<grid_for(BQ), 256, 0, st>>>(U, adv_in, P, SH, V, BQ);
+      ew_launch(k_row0_coarse_halo, dim3(grid_for(BQ)), 256, st, U, adv_in, P, SH, V, BQ);
     });
   }
   Fam f;
@@ -1637,11 +1683,11 @@ int local_coarse_source(const lmg_system& S, int B, int c, const double* U, cons
   TRY(family(Sc, B, E_COARSE, f, st));
   if (is_first) {
     TRY(launch(CLS_ELEM, 0.0, 24.0 * BQ, st, [&] {
-      k_row0_coarse<<<grid_for(BQ), 256, 0, st>>>(U, src, SH, V, BQ);
+      ew_launch(k_row0_coarse, dim3(grid_for(BQ)), 256, st, U, src, SH, V, BQ);
     }));
   } else {
     TRY(launch(CLS_ELEM, 0.0, 32.0 * BQ, st, [&] {
-      k_row0_coarse_halo<<<grid_for(BQ), 256, 0, st>>>(U, adv_in, P, SH, V, BQ);
+      ew_launch(k_row0_coarse_halo, dim3(grid_for(BQ)), 256, st, U, adv_in, P, SH, V, BQ);
     }));
   }
   return LMG_OK;
@@ -1650,7 +1696,7 @@ int local_coarse_source(const lmg_system& S, int B, int c, const double* U, cons
 int local_correct(int nb, int B, int q, int c, double* U, const double* V, cudaStream_t st) {
   const int64_t BQ = (int64_t)B * q;
   return launch(CLS_ELEM, 0.0, 24.0 * nb * BQ, st, [&] {
-    k_correct<<<grid_for((int64_t)nb * BQ), 256, 0, st>>>(U, c * BQ, V, BQ, nb, BQ);
+    ew_launch(k_correct, dim3(grid_for((int64_t)nb * BQ)), 256, st, U, c * BQ, V, BQ, nb, BQ);
   });
 }
 
@@ -1672,7 +1718,7 @@ int local_residual_post(const lmg_system& S, int B, int c, const double* U, cons
   double* fpart = work;
   double* cpart = work + (size_t)nb * nt * B;
   TRY(launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
-    k_cpart<<<dim3(B, nb), 256, 0, st>>>(U, P, src, is_first ? 1 : 0, c, B, q, cpart);
+    ew_launch(k_cpart, dim3(dim3(B, nb)), 256, st, U, P, src, is_first ? 1 : 0, c, B, q, cpart);
   }));
   Fam f;  // rows kc+1, k = 0..nb-1
   f.ntasks = nb; f.blk0 = 0; f.blk_step = c;
@@ -1683,7 +1729,7 @@ int local_residual_post(const lmg_system& S, int B, int c, const double* U, cons
   f.part = fpart; f.slot0 = 0;
   TRY(family(S, B, E_RESID, f, st));
   return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
-    k_combine_post<<<(int)(((int64_t)nb * B + 255) / 256), 256, 0, st>>>(cpart, fpart, nb, nt, B,
+    ew_launch(k_combine_post, dim3((int)(((int64_t)nb * B + 255) / 256)), 256, st, cpart, fpart, nb, nt, B,
                                                                           block_part);
   });
 }
@@ -1727,23 +1773,23 @@ int local_residual_full_b(const lmg_system& S, int B, int c, const double* U, co
   if (!is_first) {
     double* row = reinterpret_cast<double*>(tmp);
     TRY(launch(CLS_ELEM, 0.0, 24.0 * BQ, st, [&] {
-      k_halo_finish<<<grid_for(BQ), 256, 0, st>>>(src, adv_in, row, BQ);
+      ew_launch(k_halo_finish, dim3(grid_for(BQ)), 256, st, src, adv_in, row, BQ);
     }));
     s0 = row;
   }
   if (is_first || is_conv(S)) {
     // the system's row 0: reduced as the single-GPU solve reduces it (residual_full)
     TRY(launch(CLS_ELEM, 0.0, 16.0 * BQ, st, [&] {
-      k_resid_row0<<<B, 256, 0, st>>>(s0, U, nullptr, r0part, 0, B, q);
+      ew_launch(k_resid_row0, dim3(B), 256, st, s0, U, nullptr, r0part, 0, B, q);
     }));
   } else {
     // an interior row of the whole system: the E_RESID tile order (bitwise the one-GPU norm)
     TRY(launch(CLS_ELEM, 0.0, 16.0 * BQ, st, [&] {
-      k_resid_row0_tiles<<<(B + 127) / 128, 128, 0, st>>>(s0, U, r0part, B, q);
+      ew_launch(k_resid_row0_tiles, dim3((B + 127) / 128), 128, st, s0, U, r0part, B, q);
     }));
   }
   return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
-    k_combine_full<<<(int)(((int64_t)nb * B + 255) / 256), 256, 0, st>>>(rpart, r0part, nb, c, nt, B,
+    ew_launch(k_combine_full, dim3((int)(((int64_t)nb * B + 255) / 256)), 256, st, rpart, r0part, nb, c, nt, B,
                                                                           block_part);
   });
 }
@@ -1754,7 +1800,7 @@ int residual_full(const lmg_system& S, int B, const double* U, const double* src
   const int q = S.width;
   const int64_t BQ = (int64_t)B * q;
   const int n = S.num_layers;
-  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_resid_row0<<<B, 256, 0, st>>>(src, U, R, part, 0, B, q); }));
+  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { ew_launch(k_resid_row0, dim3(B), 256, st, src, U, R, part, 0, B, q); }));
   Fam f;
   f.ntasks = n - 1; f.blk0 = 0; f.blk_step = 1;
   f.x = U; f.x_ts = BQ;
@@ -1768,7 +1814,7 @@ int residual_full(const lmg_system& S, int B, const double* U, const double* src
 }
 
 int reduce_norms(const double* part, int64_t nslots, int B, double* norms, cudaStream_t st) {
-  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_reduce_norms<<<(B + 127) / 128, 128, 0, st>>>(part, nslots, B, norms); }));
+  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { ew_launch(k_reduce_norms, dim3((B + 127) / 128), 128, st, part, nslots, B, norms); }));
   return LMG_OK;
 }
 
@@ -1835,7 +1881,7 @@ int layout_ws(const lmg_system& fine, int nlevels, int c, int B, char* base, Wor
 
 int norms_from_blocks(const double* block_part, int nblocks, int B, double* norms, cudaStream_t st) {
   return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
-    k_reduce_norms<<<(B + 127) / 128, 128, 0, st>>>(block_part, nblocks, B, norms);
+    ew_launch(k_reduce_norms, dim3((B + 127) / 128), 128, st, block_part, nblocks, B, norms);
   });
 }
 
@@ -2024,7 +2070,7 @@ int lmg_assemble_coarse_source(const lmg_system* coarse, int B, const double* UH
   TRY(check_sys(coarse, B));
   const int64_t BQ = (int64_t)B * coarse->width;
   // row 0: propagation_operator row 0 (U_H[0]) plus the residual row 0
-  TRY(launch(CLS_ELEM, 0.0, 0.0, S_(stream), [&] { k_add<<<grid_for(BQ), 256, 0, S_(stream)>>>(out, UH, RH, BQ); }));
+  TRY(launch(CLS_ELEM, 0.0, 0.0, S_(stream), [&] { ew_launch(k_add, dim3(grid_for(BQ)), 256, S_(stream), out, UH, RH, BQ); }));
   Fam f;
   f.ntasks = coarse->num_layers - 1;
   f.x = UH; f.x_ts = BQ;
@@ -2513,7 +2559,7 @@ int lmg_local_fcf_fused(const lmg_system* sys, int B, int c, double* U, const do
 int lmg_halo_finish(const double* s0, const double* adv_in, double* out, int64_t len, void* stream) {
   cudaStream_t st = S_(stream);
   return launch(CLS_ELEM, 0.0, 24.0 * len, st, [&] {
-    k_halo_finish<<<grid_for(len), 256, 0, st>>>(s0, adv_in, out, len);
+    ew_launch(k_halo_finish, dim3(grid_for(len)), 256, st, s0, adv_in, out, len);
   });
 }
 
@@ -2626,7 +2672,7 @@ int lmg_l2_norms(const double* x, int n, int B, int q, double* norms, void* work
   double* part = reinterpret_cast<double*>(work);
   const int64_t BQ = (int64_t)B * q;
   for (int j = 0; j < n; ++j) {  // one slot per row: sum_b of row j (zero source minus -x)
-    TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { k_resid_row0<<<B, 256, 0, st>>>(x + j * BQ, nullptr, nullptr, part, j, B, q); }));
+    TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { ew_launch(k_resid_row0, dim3(B), 256, st, x + j * BQ, nullptr, nullptr, part, j, B, q); }));
   }
   return reduce_norms(part, n, B, norms, st);
 }

@@ -139,7 +139,10 @@ static __device__ const double2 kTanhExp2[64] = {  // {hi, lo}: 2^(j/64) = hi + 
     {0x1.f50765b6e4540p+0, 0x1.9d3e12dd8a18bp-54},
     {0x1.fa7c1819e90d8p+0, 0x1.74853f3a5931ep-55}};
 
-__device__ __forceinline__ double fast_tanh(double x) {
+// TL: the table lookup (global __ldg here; the latency-bound warp sweep reads a shared-memory
+// copy so the lookup is not an L2 round trip on every step of its serial chain)
+template <class TL>
+__device__ __forceinline__ double fast_tanh_impl(double x, TL tl) {
   x = x > 20.0 ? 20.0 : x;  // |tanh| rounds to 1 beyond 19.06; comparisons keep NaN
   x = x < -20.0 ? -20.0 : x;
   const double kMagic = 6755399441055744.0;  // 1.5 * 2^52: rint by addition
@@ -155,7 +158,7 @@ __device__ __forceinline__ double fast_tanh(double x) {
   p = fma(rh, p, 2.0);
   const double q = rh * p;                // e^(2 rh) - 1
   const double sc = __hiloint2double((1023 + (ni >> 6)) << 20, 0);  // 2^m
-  const double2 T = __ldg(&kTanhExp2[ni & 63]);
+  const double2 T = tl(ni & 63);
   const double sT = sc * T.x;  // exact
   // sT - 1 is exact when m = 0; the table's low part keeps em1 accurate where it cancels
   const double em1 = fma(sT, q, fma(sc, T.y, sT - 1.0));
@@ -167,6 +170,10 @@ __device__ __forceinline__ double fast_tanh(double x) {
   double t = em1 * y;
   t = fma(fma(-d, t, em1), y, t);
   return copysign(t, x);  // odd: keeps the sign of -0.0 (numpy's tanh(-0.0) = -0.0)
+}
+
+__device__ __forceinline__ double fast_tanh(double x) {
+  return fast_tanh_impl(x, [](int i) { return __ldg(&kTanhExp2[i]); });
 }
 
 __device__ __forceinline__ double act_fwd(int a, double v) {

@@ -399,6 +399,183 @@ using Cfg128A = SwCfg<128, 1, 4, true, 16>;
 using Cfg16F = SwCfg<16, 1, 6, false, 16>;
 using Cfg16A = SwCfg<16, 1, 6, true, 16>;
 
+// ------------------------------------------------------------------------------------------
+// Warp-level FMA sweep (cfg WSWEEP): narrow networks, q <= 32 -- a layer step is a q x q matvec
+// per sample (a few hundred flops), far too small for tensor-core tiles and a cluster
+// all-gather per step (north_star: "warp-level FMA paths otherwise").  One CTA per (chain,
+// group of up to WPB samples), one warp per sample; lane i holds state column i in a register
+// for all of the chain's steps.  The serial chain is latency-bound, so nothing the step needs
+// may be a global round trip: every operand of step s -- W block, bias row, source and act'
+// rows of the CTA's samples -- streams through a per-CTA cp.async ring WST-1 steps ahead, and
+// the tanh table sits in shared memory.  W rows are padded to KM+1 doubles so both the forward
+// (lane i reads row i) and the adjoint (lane n reads column n) fragments are conflict-free.
+// The step: pre_i = sum_k W[i][k] x_k as ONE k-ascending FMA chain (x_k broadcast by shuffles)
+// -- bitwise what one DMMA m8n8k4 chain computes (tools/dmma_fma_probe.cu: 0 mismatches in 4M
+// outputs), so this path is bitwise the per-step and cluster paths -- then the E_PROP epilogue
+// with the reference's rounding.  Same chains, destinations and transient rows as sweep_kernel.
+constexpr int WST = 4;
+constexpr int WPB_MAX = 8;
+
+// one ring stage: W block (forward stored transposed, so both directions read [k][lane]), bias
+// row, the CTA's source rows and act' rows
+template <int KM>
+struct WStage {
+  static constexpr int W = 0, BIAS = KM * KM, SRC = BIAS + KM, D = SRC + WPB_MAX * KM;
+  static constexpr int SIZE = D + WPB_MAX * KM;  // doubles
+};
+
+template <int KM, bool ADJ>
+__global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
+  using SG = WStage<KM>;
+  constexpr int QQ = KM * KM;
+  extern __shared__ double wsm[];  // [64] double2 tanh table | [WST][SG::SIZE] ring
+  double2* tab = reinterpret_cast<double2*>(wsm);
+  double* ring = wsm + 128;
+  const int k = a.k0 + (int)blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = (int)(blockDim.x >> 5);
+  const int b0 = (int)blockIdx.x * nw;
+  const int b = b0 + warp;  // this warp's sample
+  const int64_t BQ = (int64_t)a.B * KM;
+  const Chain ch = chain_of(a, k, BQ);
+  if (ch.nsteps <= 0) return;  // uniform over the CTA
+  const bool on = b < a.B && lane < KM;  // warps beyond the batch still load and synchronise
+  const int li = lane & (KM - 1);
+  const int nthr = (int)blockDim.x, tid = (int)threadIdx.x;
+  const int nwb = min(nw, a.B - b0) * KM;  // source / act' elements of this CTA's live samples
+  const bool dense_src = a.src && !a.src_head;
+  const bool has_b = !ADJ && a.bias;
+  const bool tanh_act = !ADJ && a.act == LMG_ACT_TANH;
+  if (tanh_act)
+    for (int i = tid; i < 64; i += nthr) tab[i] = kTanhExp2[i];
+  // programmatic dependent launch: everything below may read upstream results (source rows
+  // written by the previous launch); dependents may launch once this grid is running
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  // operand streams of step s (row j = r0 + 1 + s, block j - 1), advanced once per loaded stage
+  const double* wl = a.W + (int64_t)ch.r0 * a.w_stride;
+  const double* bl = has_b ? a.bias + (int64_t)ch.r0 * a.b_stride : nullptr;
+  const double* sl = dense_src ? a.src + (int64_t)(ch.r0 + 1) * BQ + (int64_t)b0 * KM : nullptr;
+  const double* dl = ADJ ? a.D + (int64_t)(ch.r0 + 1) * a.d_stride + (int64_t)b0 * KM : nullptr;
+  int loaded = 0;
+  auto load_next = [&]() {  // everything step `loaded` reads -> slot loaded % WST
+    if (loaded < ch.nsteps) {
+      double* dst = ring + (loaded % WST) * SG::SIZE;
+      for (int e = tid; e < QQ; e += nthr) {
+        const int r = e / KM, cc = e % KM;  // W[r][cc]
+        cp_async<1>(dst + SG::W + (ADJ ? e : cc * KM + r), wl + e, true);
+      }
+      if (has_b && tid < KM) cp_async<1>(dst + SG::BIAS + tid, bl + tid, true);
+      if (dense_src)
+        for (int e = tid; e < nwb; e += nthr) cp_async<1>(dst + SG::SRC + e, sl + e, true);
+      if (ADJ && loaded + 1 < ch.nsteps)  // act' of row j scales the next step's operand
+        for (int e = tid; e < nwb; e += nthr) cp_async<1>(dst + SG::D + e, dl + e, true);
+      wl += a.w_stride;
+      if (has_b) bl += a.b_stride;
+      if (dense_src) sl += BQ;
+      if (ADJ) dl += a.d_stride;
+    }
+    ++loaded;
+    cp_commit();
+  };
+#pragma unroll
+  for (int s = 0; s < WST - 1; ++s) load_next();
+
+  // x: the state (unscaled); xa: the A operand (adjoint: D_row * m)
+  double x = 0.0, xa = 0.0;
+  if (on) {
+    x = ch.start[(int64_t)b * KM + lane];
+    xa = ADJ ? __dmul_rn(x, a.D[(int64_t)ch.r0 * a.d_stride + (int64_t)b * KM + lane]) : x;
+  }
+  const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0;
+  for (int s = 0; s < ch.nsteps; ++s) {
+    const int j = ch.r0 + 1 + s;  // row produced, with block j-1
+    const bool last = s + 1 == ch.nsteps;
+    if (tr) a.trace[4 * s] = gtimer();
+    cp_wait<WST - 2>();  // this thread's copies of stage s landed
+    __syncthreads();     // ... and everyone's; every warp is done with slot (s-1) % WST
+    if (tr) a.trace[4 * s + 1] = gtimer();
+    load_next();
+    const double* st = ring + (s % WST) * SG::SIZE;
+    const double bia = has_b ? st[SG::BIAS + li] : 0.0;
+    const double sv = dense_src ? st[SG::SRC + warp * KM + li] : 0.0;
+    const double dn = (ADJ && !last) ? st[SG::D + warp * KM + li] : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KM; ++kk) {
+      const double xk = __shfl_sync(0xffffffffu, xa, kk);
+      acc = fma(st[SG::W + kk * KM + li], xk, acc);
+    }
+    if (tr) a.trace[4 * s + 2] = gtimer();
+    double pre = acc;
+    if (has_b) pre = __dadd_rn(pre, bia);
+    double v = pre;
+    if (!ADJ) v = tanh_act ? fast_tanh_impl(pre, [&](int i) { return tab[i]; }) : act_fwd(a.act, pre);
+    const double adv = __dadd_rn(x, __dmul_rn(a.h, v));
+    const double o = __dadd_rn(dense_src ? sv : 0.0, adv);
+    if (on) {
+      double* out = dest_of(a, k, j, BQ);
+      if (out) out[(int64_t)b * KM + lane] = o;
+      if (a.mode == SW_FCF && a.advH && j == k * a.c + 1)
+        a.advH[(int64_t)k * BQ + (int64_t)b * KM + lane] = __dadd_rn(x, __dmul_rn(a.h2, v));
+    }
+    x = o;
+    xa = ADJ ? __dmul_rn(o, dn) : o;
+    if (tr) a.trace[4 * s + 3] = gtimer();
+  }
+}
+
+template <int KM>
+size_t wsweep_smem() { return sizeof(double) * (128 + (size_t)WST * WStage<KM>::SIZE); }
+
+int wsweep_wpb(int B) { return B >= WPB_MAX ? WPB_MAX : B; }  // warps (samples) per CTA
+
+bool wsweep_enabled() {
+  static const bool off = getenv("LMG_NO_WSWEEP") != nullptr;
+  return !off;
+}
+
+template <int KM, bool ADJ>
+cudaError_t wsweep_attr() {
+  static const cudaError_t e = cudaFuncSetAttribute(
+      wsweep_kernel<KM, ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsweep_smem<KM>());
+  return e;
+}
+
+template <int KM, bool ADJ>
+int wsweep_occupancy() {
+  int per = 0;
+  if (wsweep_attr<KM, ADJ>() != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, wsweep_kernel<KM, ADJ>, 32 * WPB_MAX,
+                                                    wsweep_smem<KM>()) != cudaSuccess)
+    return 0;
+  return per;
+}
+
+template <int KM, bool ADJ>
+cudaError_t wlaunch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
+  const cudaError_t e = wsweep_attr<KM, ADJ>();
+  if (e != cudaSuccess) return e;
+  static const bool pdl_on = getenv("LMG_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(s.grid.y, s.grid.z, 1);
+  cfg.blockDim = dim3(s.nthreads, 1, 1);
+  cfg.dynamicSmemBytes = s.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, wsweep_kernel<KM, ADJ>, a);
+}
+
+cudaError_t wsweep_launch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
+  if (a.q <= 16) return a.adj ? wlaunch<16, true>(a, s, st) : wlaunch<16, false>(a, s, st);
+  return a.adj ? wlaunch<32, true>(a, s, st) : wlaunch<32, false>(a, s, st);
+}
+
 // run f with the configuration tag of (cfg, adjoint)
 template <class F>
 auto with_cfg(int cfg, bool adj, F&& f) {
@@ -501,6 +678,9 @@ int sweep_config(int q, int B, int adj, int nchains) {
     const char* e = getenv("LMG_SWEEP_CFG");
     return e ? atoi(e) : -1;
   }();
+  // narrow networks: the warp-level FMA sweep (one k-ascending chain per output, like cfg 0)
+  if ((q == 16 || q == 32) && wsweep_enabled() && (forced_env < 0 || forced_env == SWEEP_CFG_WARP))
+    return SWEEP_CFG_WARP;
   const bool ok64 = adj ? fits<Cfg64A>(q) : fits<Cfg64F>(q);
   if (canonical_order()) return ok64 ? 0 : -1;  // one k-ascending chain or the per-step path
   const int forced = forced_env;
@@ -518,6 +698,21 @@ int sweep_shape(const SweepArgs& a, SweepShape* s, int forced_cfg) {
   const int nchains = a.mode == SW_SEQ ? 1 : (a.nchains > 0 ? a.nchains : a.n / a.c);
   const int mt = (a.B + SW_BM - 1) / SW_BM;
   int cfg = sweep_config(a.q, a.B, a.adj, nchains);
+  if (forced_cfg == SWEEP_CFG_WARP) {
+    if (a.q != 16 && a.q != 32) return -1;
+    cfg = SWEEP_CFG_WARP;
+  } else if (cfg == SWEEP_CFG_WARP && forced_cfg >= 0) {
+    cfg = -1;  // a cluster configuration was asked for: the generic selection below
+  }
+  if (cfg == SWEEP_CFG_WARP) {
+    const int wpb = wsweep_wpb(a.B);
+    s->cfg = cfg;
+    s->cs = 1;
+    s->nthreads = 32 * wpb;
+    s->smem = a.q <= 16 ? wsweep_smem<16>() : wsweep_smem<32>();
+    s->grid = dim3(1, (a.B + wpb - 1) / wpb, nchains);
+    return 0;
+  }
   if (forced_cfg >= 0) {
     const bool ok = with_cfg(forced_cfg, a.adj, [&](auto c) { return fits<decltype(c)>(a.q); });
     if (ok) cfg = forced_cfg;
@@ -537,11 +732,23 @@ int sweep_shape(const SweepArgs& a, SweepShape* s, int forced_cfg) {
 }
 
 cudaError_t sweep_launch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
+  if (s.cfg == SWEEP_CFG_WARP) return wsweep_launch(a, s, st);
   return with_cfg(s.cfg, a.adj, [&](auto c) { return launch_c<decltype(c)>(a, s, st); });
 }
 
 // how many clusters of a configuration can be co-resident (cudaOccupancyMaxActiveClusters)
 int sweep_max_clusters(int q, int adj, int cfg) {
+  if (cfg == SWEEP_CFG_WARP) {
+    // independent CTAs, no co-residency needed: allow a few waves of 8-warp CTAs (each CTA runs
+    // a whole chain, so a second wave costs one more chain's latency, still far below per-step
+    // launches)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per = q <= 16 ? (adj ? wsweep_occupancy<16, true>() : wsweep_occupancy<16, false>())
+                            : (adj ? wsweep_occupancy<32, true>() : wsweep_occupancy<32, false>());
+    return 4 * per * sms;
+  }
   SweepArgs a{};
   a.mode = SW_SEQ; a.B = 16; a.q = q; a.n = 2; a.adj = adj;
   SweepShape sh;

@@ -19,7 +19,8 @@
 namespace lmg {
 
 // Canonical summation order (lmg_set_canonical_order): every layer step is one k-ascending DMMA
-// chain per output -- the 64-column sweep configuration only, no split-K serial steps -- so the
+// (or, bitwise the same, FMA) chain per output -- the 64-column sweep configuration or the warp
+// FMA sweep only, no split-K serial steps -- so the
 // results are bitwise independent of batch size, partition and routing (defined in lmg.cu).
 bool canonical_order();
 
@@ -55,6 +56,9 @@ struct SweepArgs {
   int nchains;  // chains in this launch (0: all nb of the level)
 };
 
+// warp-level FMA sweep for narrow networks (q <= 32; lmg_sweep.cu wsweep_kernel): no clusters,
+// grid (1, batch groups of 8 samples, chains)
+constexpr int SWEEP_CFG_WARP = 4;
 // configuration the launcher would use for (q, B, adj), or -1 if the fused sweep cannot run it
 int sweep_config(int q, int B, int adj, int nclusters_hint);
 // dynamic shared memory, cluster size and grid of a config

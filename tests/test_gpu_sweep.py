@@ -5,6 +5,8 @@ FAS training step (forward solve, FAS adjoint, gradients + SGD) and a serial pro
   output) is BITWISE identical to the per-step kernels (LMG_NO_SWEEP=1);
 * the default k-split configuration (two warps per output tile, partials summed in fixed order)
   matches within the parity tolerance, with identical cycle counts;
+* narrow networks (q <= 32) default to the warp-level FMA sweep, which is BITWISE the per-step
+  kernels too (tools/dmma_fma_probe.cu: a DMMA m8n8k4 chain is a k-ascending FMA chain);
 * the fused runs launch fewer kernels."""
 
 import os
@@ -62,6 +64,10 @@ def test_fused_sweep_matches_per_step(case, tmp_path):
         assert on[key].shape == off[key].shape, key
         assert _close(on[key], off[key], rel), (key, float(np.nanmax(np.abs(on[key] - off[key]))))
     assert int(on["launches"]) <= int(off["launches"])  # B > 144: no fused launch applies
+    from paper_2007_07336_b200._lib import ROUTES
+    if case[1] <= 32:  # narrow networks run the warp-level FMA sweep by default
+        assert on["routes"][ROUTES.index("wsweep")] > 0
+        assert off["routes"][ROUTES.index("wsweep")] == 0
     # the other shapes, forced: 32 columns / 16-CTA clusters (k split over warp pairs) and
     # 128 columns / 4-CTA clusters (serial solves of many batch tiles)
     forced = ["1"] + (["2"] if case[1] % 128 == 0 and case[1] <= 512 else [])
@@ -72,8 +78,12 @@ def test_fused_sweep_matches_per_step(case, tmp_path):
         for key, rel in (("U1", 1e-12), ("lam", 1e-12), ("W", 1e-12), ("Us", 1e-12),
                          ("hist", 1e-9), ("adj_hist", 1e-9)):
             assert _close(f[key], off[key], rel), (cfg, key)
-    if case[1] % 64 == 0:  # one-chain configuration: bitwise (the serial split-K path is not)
-        one = _run(case, tmp_path, {"LMG_SWEEP_CFG": "0", "LMG_NO_SPLITK": "1"})
+    if case[1] % 64 == 0 or case[1] <= 32:
+        # one-chain configurations: bitwise (the serial split-K path is not) -- the 64-column
+        # cluster sweep, and for narrow networks the default warp-level FMA sweep (one FMA chain
+        # over k ascending per output is what a DMMA m8n8k4 chain computes, bit for bit)
+        one = _run(case, tmp_path, {"LMG_SWEEP_CFG": "0" if case[1] % 64 == 0 else "4",
+                                    "LMG_NO_SPLITK": "1"})
         off = _run(case, tmp_path, {"LMG_NO_SWEEP": "1", "LMG_NO_SPLITK": "1"})  # one chain too
         for key in ("U0", "hist", "cyc", "U1", "lam", "loss", "adj_hist", "adj_cyc", "W", "b"):
             assert np.array_equal(one[key], off[key], equal_nan=True), key

@@ -70,9 +70,12 @@ if __name__ == "__main__":
     main()
 
 
-def trace(N=None, q=512, B=None):
-    """Per-step phase times of one serial fused sweep (lmg_debug_sweep_trace)."""
+def trace(N=None, q=None, B=None):
+    """Per-step phase times of one serial fused sweep (lmg_debug_sweep_trace).  Cluster sweeps
+    stamp (start, peers' state landed, mainloop done, epilogue done); the warp FMA sweep (q 16 /
+    32) stamps (start, W stage landed, matvec done, epilogue done)."""
     N = N or int(os.environ.get("LMG_TRACE_N", 1024))
+    q = q or int(os.environ.get("LMG_TRACE_Q", 512))
     B = B or int(os.environ.get("LMG_TRACE_B", 16))
     import ctypes
 
