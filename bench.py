@@ -56,6 +56,12 @@ CONFIGS = {
     "c6": dict(depth=1024, width=16, batch=1, cf=16, threshold=4, tol=1e-9, max_cycles=50, lr=0.1,
                workload="dense tanh ResNet 1024 layers width 16 batch 1, 3-level FAS cf 16 "
                         "(levels [1024,64,4]) forward+adjoint training step to tol 1e-9"),
+    # the same regime four times deeper (tools/cf_sweep.py --depths: FAS's per-cycle critical path
+    # grows with the level count, serial propagation with the depth) -- where the FAS step is
+    # faster than layer-by-layer GPU propagation on one GPU
+    "c7": dict(depth=4096, width=16, batch=1, cf=16, threshold=16, tol=1e-9, max_cycles=50, lr=0.1,
+               workload="dense tanh ResNet 4096 layers width 16 batch 1, 3-level FAS cf 16 "
+                        "(levels [4096,256,16]) forward+adjoint training step to tol 1e-9"),
 }
 
 METRIC = "FAS fwd+adjoint solve time to tol; layer*samples/s"

@@ -15,6 +15,8 @@ same seeded inputs:
   c2_depth64   the c2 shape at depth 64 ([64,16,4]) solved to tol 1e-9 (same kernels, full
                convergence, cycle counts compared).
   c4_depth32   the c4 width (q 1024) at depth 32 ([32, 8]), B 128.
+  c6_full / c7_full / c1_full  the narrow bench shapes (q 16 at depth 1024 and 4096, q 32): the
+               warp-level FMA sweeps for every relaxed level and serial solve.
   c3_depth32   the c3 conv geometry (64 channels, 32 x 32 rasters, relu) at depth 32 ([32,8,2]), B 2:
                implicit-GEMM conv kernels at C = 64 (unpadded tiles, the 3-stage adjoint ring).
 
@@ -47,9 +49,11 @@ CASES = {  # name: (N, q, B, c, threshold, max_cycles, kernel variants that must
     "c2_depth64": (64, 512, 256, 4, 4, 50, ("step_small_full", "step_wide_full", "serial_splitk")),
     "c4_depth32": (32, 1024, 128, 4, 8, 50, ("step_small_full", "step_wide_full")),
     # bench c6: BASELINE configs[4]'s shortest-critical-path point (q 16, one sample, cf 16)
-    "c6_full": (1024, 16, 1, 16, 4, 50, ("sweep_fcf", "sweep_seq")),
-    # bench c1: the reference demo's shape
-    "c1_full": (64, 32, 64, 4, 16, 50, ()),
+    "c6_full": (1024, 16, 1, 16, 4, 50, ("sweep_fcf", "sweep_seq", "wsweep")),
+    # bench c7: the deep narrow network (4096 x 16, cf 16, [4096, 256, 16]) -- warp FMA sweeps
+    "c7_full": (4096, 16, 1, 16, 16, 50, ("sweep_fcf", "sweep_seq", "wsweep")),
+    # bench c1: the reference demo's shape (q 32: the 32-column warp FMA sweeps)
+    "c1_full": (64, 32, 64, 4, 16, 50, ("wsweep",)),
 }
 
 

@@ -35,7 +35,7 @@ from paper_2007_07336_b200.training import _dense_apply, backward  # noqa: E402
 N = 1024
 
 
-def hierarchies():
+def hierarchies(N=1024):
     for cf in (2, 4, 8, 16):
         for L in range(2, 7):
             if cf ** (L - 1) > N or N % cf ** (L - 1):
@@ -62,7 +62,7 @@ def timed(fn, steps, restore):
     return float(np.median(out)), r
 
 
-def run_point(q, B, cf, sizes, steps):
+def run_point(q, B, cf, sizes, steps, N=N):
     dev = torch.device("cuda", 0)
     d = P.device_network(N, q, [0, N, q], device=dev)
     saved = [x.clone() for x in (d.stack.W, d.stack.b, d.Wo, d.bo, d.Wr, d.br)]
@@ -105,15 +105,29 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r2_cf_sweep.json"))
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--shapes", default="512x16,16x1")
+    ap.add_argument("--depths", default="1024",
+                    help="comma list of N; with --cf/--levels a depth sweep of one hierarchy shape")
+    ap.add_argument("--cf", type=int, default=None)
+    ap.add_argument("--levels", default=None, help="comma list of level counts (with --cf)")
     a = ap.parse_args()
     rows = []
+
+    def points(n):
+        if a.cf is None:
+            yield from hierarchies(n)
+            return
+        for L in (int(v) for v in a.levels.split(",")):
+            if a.cf ** (L - 1) <= n and n % a.cf ** (L - 1) == 0:
+                yield a.cf, L, [n // a.cf ** l for l in range(L)]
+
     for shape in a.shapes.split(","):
         q, B = (int(v) for v in shape.split("x"))
-        for cf, L, sizes in hierarchies():
+        for n, (cf, L, sizes) in ((n, p) for n in (int(v) for v in a.depths.split(",")) for p in points(n)):
             t0 = time.time()
-            r = run_point(q, B, cf, sizes, a.steps)
+            r = run_point(q, B, cf, sizes, a.steps, N=n)
+            r["depth"] = n
             rows.append(r)
-            print(f"q {q} B {B} cf {cf:2d} levels {sizes}: cycles {r['fwd_cycles']}+{r['adj_cycles']} "
+            print(f"N {n} q {q} B {B} cf {cf:2d} levels {sizes}: cycles {r['fwd_cycles']}+{r['adj_cycles']} "
                   f"step {r['gpu_ms_per_step']:.2f} ms serial {r['serial_gpu_ms_per_step']:.2f} ms "
                   f"crit {r['critical_path_total']} ({time.time() - t0:.1f}s)", flush=True)
             torch.cuda.empty_cache()
