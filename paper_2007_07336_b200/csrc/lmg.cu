@@ -279,6 +279,32 @@ __global__ void k_fcf_commit(double* __restrict__ U, const double* __restrict__ 
   }
 }
 
+// k_fcf_commit + k_coarse_from_adv + k_row0_coarse in one pass (single GPU, first rank): the
+// new C rows are committed and the coarse source assembled from them with the same operations
+//   U[0] = f[0],  S_H[0] = U[0] + (f[0] - U[0]),  V[0] = U[0]
+//   U[nc] = Cn[n], S_H[n] = (U[nc] - advH[n-1]) + (P[n] - U[nc]),  V[n] = U[nc]   (n >= 1)
+__global__ void k_commit_coarse(double* __restrict__ U, const double* __restrict__ src0,
+                                const double* __restrict__ Cn, const double* __restrict__ adv,
+                                const double* __restrict__ P, double* __restrict__ SH,
+                                double* __restrict__ V, int nb, int c, int64_t BQ) {
+  pdl_enter();
+  const int64_t total = (int64_t)nb * BQ;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / BQ, i = e - r * BQ;
+    double y;
+    if (r == 0) {
+      y = src0[i];
+      SH[i] = __dadd_rn(y, __dadd_rn(src0[i], -y));
+    } else {
+      y = Cn[e];
+      SH[e] = __dadd_rn(__dadd_rn(y, -adv[e - BQ]), __dadd_rn(P[e], -y));
+    }
+    U[r * c * BQ + i] = y;
+    if (V) V[e] = y;
+  }
+}
+
 // coarse FAS source rows n >= 1 from the advance computed in the F sweep:
 //   S_H[n] = (U[nc] - advH[n-1]) + (P[n] - U[nc]),  V[n] = U[nc]      (multigrid.py:142)
 __global__ void k_coarse_from_adv(const double* __restrict__ Uc, int64_t u_ts,
@@ -326,6 +352,37 @@ __global__ void k_cpart(const double* __restrict__ U, const double* __restrict__
   double acc = 0.0;
   for (int i = threadIdx.x; i < q; i += blockDim.x) {
     double r = __dadd_rn(p ? p[i] : 0.0, -u[i]);
+    acc = fma(r, r, acc);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cpart[(int64_t)k * B + b] = sh[0];
+}
+
+// k_correct + k_cpart in one pass (the finest level of a single-GPU cycle): the correction
+// U[kc] += V[k] - U[kc] (multigrid.py:227), then the C-row residual partial of the corrected row
+// with k_cpart's summation order
+__global__ void k_correct_cpart(double* __restrict__ U, const double* __restrict__ V,
+                                const double* __restrict__ P, const double* __restrict__ S0,
+                                int is_first, int c, int B, int q, double* __restrict__ cpart) {
+  pdl_enter();
+  __shared__ double sh[256];
+  const int k = blockIdx.y, b = blockIdx.x;
+  const int64_t BQ = (int64_t)B * q;
+  double* u = U + (int64_t)k * c * BQ + (int64_t)b * q;
+  const double* v = V + (int64_t)k * BQ + (int64_t)b * q;
+  const double* p = (k == 0 && is_first) ? (S0 ? S0 + (int64_t)b * q : nullptr)
+                                         : P + (int64_t)k * BQ + (int64_t)b * q;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < q; i += blockDim.x) {
+    const double u0 = u[i];
+    const double u1 = __dadd_rn(u0, __dadd_rn(v[i], -u0));
+    u[i] = u1;
+    double r = __dadd_rn(p ? p[i] : 0.0, -u1);
     acc = fma(r, r, acc);
   }
   sh[threadIdx.x] = acc;
@@ -1348,7 +1405,10 @@ int seq_sweep(const lmg_system& S, int B, const double* src, int mode, double* U
   }
   if ((int)sh.grid.y > sweep_clusters(S.width, a.adj, sh.cfg)) return -1;
   const int64_t BQ = (int64_t)B * S.width;
-  TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]
+  if (sh.cfg == SWEEP_CFG_WARP)
+    a.write_row0 = 1;  // the warp sweep stores states[0] itself (one launch fewer per solve)
+  else
+    TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]
   return run_sweep(a, sh, S.num_layers - 1, S.num_layers - 1, st);
 }
 
@@ -1356,7 +1416,8 @@ int seq_sweep(const lmg_system& S, int B, const double* src, int mode, double* U
 // the commit of the new C rows; -1 when not eligible.  Same outputs as local_fcf_a + local_fcf_b
 // on a single GPU (is_first, no next rank).
 int fcf_sweep(const lmg_system& S, int B, int c, double* U, const double* src, int mode, double* P,
-              double* advH, double* Cn, const double* Q, cudaStream_t st) {
+              double* advH, double* Cn, const double* Q, cudaStream_t st, double* SH = nullptr,
+              double* Vc = nullptr) {
   if (!Cn || !P || !src || B > sweep_max_batch() || !sweep_basic_ok(S)) return -1;
   if (!aligned16(src) || !aligned16(U) || !aligned16(Q) || !aligned16(P) || !aligned16(advH) ||
       !aligned16(Cn))
@@ -1382,6 +1443,11 @@ int fcf_sweep(const lmg_system& S, int B, int c, double* U, const double* src, i
   if (advH) written += nb;
   TRY(run_sweep(a, sh, steps, written, st));
   const int64_t BQ = (int64_t)B * S.width;
+  if (SH && advH)  // the commit and the level's coarse FAS source in one pass
+    return launch(CLS_ELEM, 0.0, 48.0 * nb * BQ, st, [&] {
+      ew_launch(k_commit_coarse, dim3(grid_for((int64_t)nb * BQ)), 256, st, U, src, Cn, advH, P, SH,
+                Vc, nb, c, BQ);
+    });
   return launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
     ew_launch(k_fcf_commit, dim3(grid_for((int64_t)nb * BQ)), 256, st, U, src, Cn, nb, c, BQ);
   });
@@ -1710,16 +1776,22 @@ size_t local_part_doubles(int L, int B, int q) {
 // the step GEMM, everything else exactly zero.  Writes canonical per-block partials nb x B.
 int local_residual_post(const lmg_system& S, int B, int c, const double* U, const double* src,
                         int mode, const double* P, bool is_first, double* block_part, double* work,
-                        double* Q, cudaStream_t st) {
+                        double* Q, cudaStream_t st, const double* Vcorr = nullptr) {
   const int q = S.width;
   const int64_t BQ = (int64_t)B * q;
   const int nb = S.num_layers / c;
   const int nt = row_slots(S);
   double* fpart = work;
   double* cpart = work + (size_t)nb * nt * B;
-  TRY(launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
-    ew_launch(k_cpart, dim3(dim3(B, nb)), 256, st, U, P, src, is_first ? 1 : 0, c, B, q, cpart);
-  }));
+  if (Vcorr)  // the correction U[kc] += V - U[kc] fused in (U is then written)
+    TRY(launch(CLS_ELEM, 0.0, 32.0 * nb * BQ, st, [&] {
+      ew_launch(k_correct_cpart, dim3(B, nb), 256, st, const_cast<double*>(U), Vcorr, P, src,
+                is_first ? 1 : 0, c, B, q, cpart);
+    }));
+  else
+    TRY(launch(CLS_ELEM, 0.0, 16.0 * nb * BQ, st, [&] {
+      ew_launch(k_cpart, dim3(dim3(B, nb)), 256, st, U, P, src, is_first ? 1 : 0, c, B, q, cpart);
+    }));
   Fam f;  // rows kc+1, k = 0..nb-1
   f.ntasks = nb; f.blk0 = 0; f.blk_step = c;
   f.x = U; f.x_ts = c * BQ;
@@ -1907,27 +1979,29 @@ int cycle(const lmg_system& S, int nlevels, int l, int c, int B, double* U, cons
   const int nb = S.num_layers / c;
   double* P = ws.P[l];
   const double* Qs = (l == 0 && q_valid) ? ws.Q : nullptr;
-  const int rs = fcf_sweep(S, B, c, U, src, mode, P, ws.advH[l], ws.Cn[l], Qs, st);
+  const lmg_system Sc = coarsen(S, c);
+  const bool coarsest = (l + 1 == nlevels - 1);
+  double* SH = ws.SH[l + 1];
+  double* V = ws.V[l + 1];
+  const int rs = fcf_sweep(S, B, c, U, src, mode, P, ws.advH[l], ws.Cn[l], Qs, st, SH,
+                           coarsest ? nullptr : V);
   if (rs < 0) {
     TRY(local_fcf_a(S, B, c, U, src, mode, true, false, Qs, st));
     TRY(local_fcf_b(S, B, c, U, src, mode, P, false, nullptr, st, ws.advH[l]));
   } else if (rs != LMG_OK) {
     return rs;
   }
-  const lmg_system Sc = coarsen(S, c);
-  const bool coarsest = (l + 1 == nlevels - 1);
-  double* SH = ws.SH[l + 1];
-  double* V = ws.V[l + 1];
-  TRY(local_coarse_source(S, B, c, U, src, mode, P, nullptr, true, SH, coarsest ? nullptr : V, st,
-                          ws.advH[l]));
+  if (rs < 0)  // (the fused sweep assembled the coarse source with its commit)
+    TRY(local_coarse_source(S, B, c, U, src, mode, P, nullptr, true, SH, coarsest ? nullptr : V, st,
+                            ws.advH[l]));
   if (coarsest)
     TRY(seq_forward(Sc, B, SH, LMG_SRC_DENSE, V, st));
   else
     TRY(cycle(Sc, nlevels, l + 1, c, B, V, SH, LMG_SRC_DENSE, ws, false, nullptr, st));
-  TRY(local_correct(nb, B, S.width, c, U, V, st));
-  if (want_norm) {
+  if (!want_norm) TRY(local_correct(nb, B, S.width, c, U, V, st));
+  if (want_norm) {  // correction fused into the C-row residual partials
     TRY(local_residual_post(S, B, c, U, src, mode, P, true, ws.block_part, ws.part,
-                            l == 0 ? ws.Q : nullptr, st));
+                            l == 0 ? ws.Q : nullptr, st, V));
     TRY(norms_from_blocks(ws.block_part, nb, B, norms, st));
   }
   return LMG_OK;

@@ -415,6 +415,7 @@ using Cfg16A = SwCfg<16, 1, 6, true, 16>;
 // with the reference's rounding.  Same chains, destinations and transient rows as sweep_kernel.
 constexpr int WST = 4;
 constexpr int WPB_MAX = 8;
+__host__ __device__ inline int wsweep_wpb(int B) { return B >= WPB_MAX ? WPB_MAX : B; }  // samples per CTA
 
 // one ring stage: W block (forward stored transposed, so both directions read [k][lane]), bias
 // row, the CTA's source rows and act' rows
@@ -424,22 +425,26 @@ struct WStage {
   static constexpr int SIZE = D + WPB_MAX * KM;  // doubles
 };
 
-template <int KM, bool ADJ>
+// V (measurement knob LMG_WSWEEP_V): 0 = next stage's copies issued before the matvec; 1 = after
+// it (the LDGSTS then queue behind the matvec's LDS instead of ahead of them); 2 = 1 + the state
+// broadcast through shared memory (LDS.128 pairs) instead of 64-bit shuffles
+template <int KM, bool ADJ, int V = 1>
 __global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
   using SG = WStage<KM>;
   constexpr int QQ = KM * KM;
-  extern __shared__ double wsm[];  // [64] double2 tanh table | [WST][SG::SIZE] ring
+  extern __shared__ double wsm[];  // [64] double2 tanh table | [WST][SG::SIZE] ring | [8][KM] x
   double2* tab = reinterpret_cast<double2*>(wsm);
   double* ring = wsm + 128;
+  double* xsh = ring + WST * SG::SIZE + (threadIdx.x >> 5) * KM;  // V 2: this warp's state row
   const int k = a.k0 + (int)blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = (int)(blockDim.x >> 5);
+  const int nw = wsweep_wpb(a.B);  // samples per CTA (blockDim is always WPB_MAX warps)
   const int b0 = (int)blockIdx.x * nw;
   const int b = b0 + warp;  // this warp's sample
   const int64_t BQ = (int64_t)a.B * KM;
   const Chain ch = chain_of(a, k, BQ);
   if (ch.nsteps <= 0) return;  // uniform over the CTA
-  const bool on = b < a.B && lane < KM;  // warps beyond the batch still load and synchronise
+  const bool on = warp < nw && b < a.B && lane < KM;  // other warps still load and synchronise
   const int li = lane & (KM - 1);
   const int nthr = (int)blockDim.x, tid = (int)threadIdx.x;
   const int nwb = min(nw, a.B - b0) * KM;  // source / act' elements of this CTA's live samples
@@ -487,27 +492,41 @@ __global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
   if (on) {
     x = ch.start[(int64_t)b * KM + lane];
     xa = ADJ ? __dmul_rn(x, a.D[(int64_t)ch.r0 * a.d_stride + (int64_t)b * KM + lane]) : x;
+    if (a.write_row0) a.U[(int64_t)b * KM + lane] = x;  // states[0] = source[0]
   }
   const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0;
   for (int s = 0; s < ch.nsteps; ++s) {
     const int j = ch.r0 + 1 + s;  // row produced, with block j-1
     const bool last = s + 1 == ch.nsteps;
-    if (tr) a.trace[4 * s] = gtimer();
+    if (tr) a.trace[4 * s] = clock64();
     cp_wait<WST - 2>();  // this thread's copies of stage s landed
     __syncthreads();     // ... and everyone's; every warp is done with slot (s-1) % WST
-    if (tr) a.trace[4 * s + 1] = gtimer();
-    load_next();
+    if (tr) a.trace[4 * s + 1] = clock64();
+    if (V == 0) load_next();
     const double* st = ring + (s % WST) * SG::SIZE;
     const double bia = has_b ? st[SG::BIAS + li] : 0.0;
     const double sv = dense_src ? st[SG::SRC + warp * KM + li] : 0.0;
     const double dn = (ADJ && !last) ? st[SG::D + warp * KM + li] : 0.0;
     double acc = 0.0;
+    if (V == 2) {
+      if (lane < KM) xsh[lane] = xa;
+      __syncwarp();
 #pragma unroll
-    for (int kk = 0; kk < KM; ++kk) {
-      const double xk = __shfl_sync(0xffffffffu, xa, kk);
-      acc = fma(st[SG::W + kk * KM + li], xk, acc);
+      for (int kk = 0; kk < KM; kk += 2) {
+        const double2 xk = *reinterpret_cast<const double2*>(xsh + kk);
+        acc = fma(st[SG::W + kk * KM + li], xk.x, acc);
+        acc = fma(st[SG::W + (kk + 1) * KM + li], xk.y, acc);
+      }
+      __syncwarp();  // the next step's store must not overtake a lagging lane's reads
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < KM; ++kk) {
+        const double xk = __shfl_sync(0xffffffffu, xa, kk);
+        acc = fma(st[SG::W + kk * KM + li], xk, acc);
+      }
     }
-    if (tr) a.trace[4 * s + 2] = gtimer();
+    if (V != 0) load_next();
+    if (tr) a.trace[4 * s + 2] = clock64();
     double pre = acc;
     if (has_b) pre = __dadd_rn(pre, bia);
     double v = pre;
@@ -522,24 +541,35 @@ __global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
     }
     x = o;
     xa = ADJ ? __dmul_rn(o, dn) : o;
-    if (tr) a.trace[4 * s + 3] = gtimer();
+    if (tr) a.trace[4 * s + 3] = clock64();
   }
 }
 
 template <int KM>
-size_t wsweep_smem() { return sizeof(double) * (128 + (size_t)WST * WStage<KM>::SIZE); }
+size_t wsweep_smem() { return sizeof(double) * (128 + (size_t)WST * WStage<KM>::SIZE + WPB_MAX * KM); }
 
-int wsweep_wpb(int B) { return B >= WPB_MAX ? WPB_MAX : B; }  // warps (samples) per CTA
+// default 1 (tools/_r2_ws_ab.sh, profiles/r2_wsweep_variants.txt: serial propagation 2.77 vs
+// 3.05 / 3.08 ms at 4096 x 16 B 1 for variants 0 / 2; at 1024 x 32 B 64 variant 2 was faster
+// alone, 1.30 vs 1.42 ms, but slower in the c1 training step)
+int wsweep_variant(int q) {
+  static const int v = [] {
+    const char* e = getenv("LMG_WSWEEP_V");
+    return e ? atoi(e) : -1;
+  }();
+  return v >= 0 ? v : 1;
+}
+
+
 
 bool wsweep_enabled() {
   static const bool off = getenv("LMG_NO_WSWEEP") != nullptr;
   return !off;
 }
 
-template <int KM, bool ADJ>
+template <int KM, bool ADJ, int V = 1>
 cudaError_t wsweep_attr() {
   static const cudaError_t e = cudaFuncSetAttribute(
-      wsweep_kernel<KM, ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsweep_smem<KM>());
+      wsweep_kernel<KM, ADJ, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsweep_smem<KM>());
   return e;
 }
 
@@ -553,9 +583,9 @@ int wsweep_occupancy() {
   return per;
 }
 
-template <int KM, bool ADJ>
-cudaError_t wlaunch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
-  const cudaError_t e = wsweep_attr<KM, ADJ>();
+template <int KM, bool ADJ, int V>
+cudaError_t wlaunch_v(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
+  const cudaError_t e = wsweep_attr<KM, ADJ, V>();
   if (e != cudaSuccess) return e;
   static const bool pdl_on = getenv("LMG_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
@@ -568,7 +598,16 @@ cudaError_t wlaunch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_on ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, wsweep_kernel<KM, ADJ>, a);
+  return cudaLaunchKernelEx(&cfg, wsweep_kernel<KM, ADJ, V>, a);
+}
+
+template <int KM, bool ADJ>
+cudaError_t wlaunch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
+  switch (wsweep_variant(KM)) {
+    case 0: return wlaunch_v<KM, ADJ, 0>(a, s, st);
+    case 2: return wlaunch_v<KM, ADJ, 2>(a, s, st);
+    default: return wlaunch_v<KM, ADJ, 1>(a, s, st);
+  }
 }
 
 cudaError_t wsweep_launch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
@@ -708,7 +747,11 @@ int sweep_shape(const SweepArgs& a, SweepShape* s, int forced_cfg) {
     const int wpb = wsweep_wpb(a.B);
     s->cfg = cfg;
     s->cs = 1;
-    s->nthreads = 32 * wpb;
+    // LMG_WSWEEP_FULLCTA=1: always 8 warps (the warps beyond the CTA's samples only share the
+    // ring copies) -- measured slower for one-sample chains (the 8-warp barrier per step costs
+    // more than the copies it spreads), so one warp per sample by default
+    static const bool full = getenv("LMG_WSWEEP_FULLCTA") != nullptr;
+    s->nthreads = 32 * (full ? WPB_MAX : wpb);
     s->smem = a.q <= 16 ? wsweep_smem<16>() : wsweep_smem<32>();
     s->grid = dim3(1, (a.B + wpb - 1) / wpb, nchains);
     return 0;

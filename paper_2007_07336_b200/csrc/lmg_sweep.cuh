@@ -54,6 +54,7 @@ struct SweepArgs {
   int k0, is_first, has_next;
   double* halo;
   int nchains;  // chains in this launch (0: all nb of the level)
+  int write_row0;  // SW_SEQ, warp FMA sweep: also store U[0] = src[0] (the solve's first row)
 };
 
 // warp-level FMA sweep for narrow networks (q <= 32; lmg_sweep.cu wsweep_kernel): no clusters,
