@@ -1316,6 +1316,7 @@ std::mutex g_graph_mu;
 std::vector<CycleGraph> g_graphs;
 unsigned long long g_graph_clock = 0;
 constexpr size_t kGraphCacheSize = 16;
+constexpr size_t kSpecMaxBytes = size_t(16) << 20;  // speculative cycles up to 16 MB of states
 
 bool sweep_disabled() {
   static const bool v = getenv("LMG_NO_SWEEP") != nullptr;
@@ -2298,6 +2299,13 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
     TRY(copy_rows(buf, q, states + (int64_t)b * q, BQ, n, q, st));
     return LMG_OK;
   };
+  auto park_from = [&](int b, const double* from) -> int {  // sample b of a (n, B, q) buffer
+    double* buf = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&buf), (size_t)n * q * sizeof(double), st));
+    parked.emplace_back(b, buf);
+    TRY(copy_rows(buf, q, from + (int64_t)b * q, BQ, n, q, st));
+    return LMG_OK;
+  };
   for (int b = 0; b < B && ndone < B; ++b)
     if (done[b]) TRY(park(b));
 
@@ -2340,9 +2348,130 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
       if (*c) cudaFreeAsync(*c, st);
     }
   } devfree{&done_d, &cyc_d, &hist_d, st};
+  int cyc = 0;
+  // one FAS cycle at the finest level: the cached cycle graph from the second cycle on
+  auto issue_cycle = [&](bool first) -> int {
+      if (use_graph && !first) {
+        if (!gexec) {
+          CycleKey key;
+          std::memset(&key, 0, sizeof(key));
+          key.fine = *fine;
+          key.nlevels = nlevels; key.c = c; key.B = B; key.src_mode = src_mode;
+          key.states = states; key.src = src; key.work = work; key.trace = g_sweep_trace;
+          {
+            std::lock_guard<std::mutex> lk(g_graph_mu);
+            for (auto& e : g_graphs)
+              if (!std::memcmp(&e.key, &key, sizeof(key))) {
+                gexec = e.exec;
+                graph_launches = e.launches;
+                e.used = ++g_graph_clock;
+                ++e.in_use;
+                break;
+              }
+          }
+          if (!gexec) {
+            cudaGraph_t graph;
+            const unsigned long long n0 = t_launches;
+            CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            int rc = cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, true);
+            cudaError_t ce = cudaStreamEndCapture(st, &graph);
+            if (rc != LMG_OK) return rc;
+            if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+            graph_launches = t_launches - n0;
+            ce = cudaGraphInstantiate(&gexec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+            g_launches -= graph_launches;  // counted per replay below
+            std::lock_guard<std::mutex> lk(g_graph_mu);
+            if (g_graphs.size() >= kGraphCacheSize) {  // evict the least recently used idle entry
+              size_t lru = g_graphs.size();
+              for (size_t i = 0; i < g_graphs.size(); ++i)
+                if (g_graphs[i].in_use == 0 && (lru == g_graphs.size() || g_graphs[i].used < g_graphs[lru].used))
+                  lru = i;
+              if (lru < g_graphs.size()) {
+                cudaGraphExecDestroy(g_graphs[lru].exec);
+                g_graphs.erase(g_graphs.begin() + lru);
+              }
+            }
+            g_graphs.push_back(CycleGraph{key, gexec, graph_launches, ++g_graph_clock, 1});
+          }
+        }
+        CUDA_TRY(cudaGraphLaunch(gexec, st));
+        g_launches += graph_launches;
+      } else {
+        TRY(cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, !first));
+      }
+    return LMG_OK;
+  };
+
+  // Speculative cycles (small states): the host's stopping test after cycle k (read-back, test,
+  // next graph launch: ~20 us of idle GPU per cycle at c6/c7) overlaps cycle k+1, already queued.
+  // Before each speculative cycle the states are snapshotted (state after cycle k); samples found
+  // converged at k are parked from the snapshot, and when the solve stops after k the snapshot is
+  // copied back -- so results, histories and cycle counts are exactly the unspeculated ones.  The
+  // price is one discarded cycle per solve plus a state copy per cycle, hence small states only.
+  // Measured SLOWER on B200 (c7 3.08 vs 2.86 ms, c6 1.85 vs 1.62 ms per training step,
+  // profiles/r2_spec_ab.txt): the discarded cycle costs more than the host turnaround it hides,
+  // which is small once the cycle is graph-replayed -- so it is opt-in (LMG_SPEC=1).
+  static const bool spec_on = getenv("LMG_SPEC") != nullptr;
+  const size_t state_bytes = (size_t)n * BQ * sizeof(double);
+  if (use_graph && !dev_loop && spec_on && state_bytes <= kSpecMaxBytes && ndone < B && max_cycles > 1) {
+    double* snap = nullptr;
+    CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&snap), state_bytes, st));
+    struct SnapFree {
+      double** p; cudaStream_t st;
+      ~SnapFree() { if (*p) cudaFreeAsync(*p, st); }
+    } snap_guard{&snap, st};
+    static thread_local double* hn = nullptr;  // pinned norms of two cycles in flight
+    static thread_local int hn_cap = 0;
+    static thread_local cudaEvent_t ev[2] = {nullptr, nullptr};
+    if (hn_cap < 2 * B) {
+      if (hn) cudaFreeHost(hn);
+      hn = nullptr;
+      hn_cap = 0;
+      CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&hn), 2 * (size_t)B * sizeof(double)));
+      hn_cap = 2 * B;
+    }
+    for (auto& e : ev)
+      if (!e) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    int issued = 0;
+    auto issue = [&]() -> int {  // cycle issued + 1, its norms into slot (issued + 1) & 1
+      if (issued > 0) TRY(copy_rows(snap, BQ, states, BQ, n, BQ, st));  // state after `issued`
+      TRY(issue_cycle(issued == 0));
+      ++issued;
+      CUDA_TRY(cudaMemcpyAsync(hn + (size_t)(issued & 1) * B, ws.norms, B * sizeof(double),
+                               cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaEventRecord(ev[issued & 1], st));
+      return LMG_OK;
+    };
+    TRY(issue());
+    for (;;) {
+      const int k = cyc + 1;  // the cycle evaluated now
+      const bool more = k < max_cycles;
+      if (more) TRY(issue());  // cycle k + 1, speculatively
+      CUDA_TRY(cudaEventSynchronize(ev[k & 1]));
+      const double* nk = hn + (size_t)(k & 1) * B;
+      cyc = k;
+      int newly = 0;
+      for (int b = 0; b < B; ++b) {
+        if (done[b]) continue;
+        hist_host[(int64_t)cyc * B + b] = nk[b];
+        cycles_host[b] = cyc;
+        if (nk[b] <= tol) { done[b] = 1; ++newly; }
+      }
+      ndone += newly;
+      if (ndone == B || !more) {
+        if (more) TRY(copy_rows(states, BQ, snap, BQ, n, BQ, st));  // undo cycle k + 1
+        break;
+      }
+      if (newly)
+        for (int b = 0; b < B; ++b)
+          if (done[b] && std::none_of(parked.begin(), parked.end(), [&](auto& pb) { return pb.first == b; }))
+            TRY(park_from(b, snap));
+    }
+  }
   std::vector<int> done_i(B);
   std::vector<double> hrows;
-  int cyc = 0;
   while (ndone < B && cyc < max_cycles) {
     if (dev_loop && cyc > 0) {
       if (!dexec) {
@@ -2414,56 +2543,7 @@ int solve_on(const lmg_system* fine, int nlevels, int c, int B, double* states,
             TRY(park(b));
       continue;
     }
-    if (use_graph && cyc > 0) {
-      if (!gexec) {
-        CycleKey key;
-        std::memset(&key, 0, sizeof(key));
-        key.fine = *fine;
-        key.nlevels = nlevels; key.c = c; key.B = B; key.src_mode = src_mode;
-        key.states = states; key.src = src; key.work = work; key.trace = g_sweep_trace;
-        {
-          std::lock_guard<std::mutex> lk(g_graph_mu);
-          for (auto& e : g_graphs)
-            if (!std::memcmp(&e.key, &key, sizeof(key))) {
-              gexec = e.exec;
-              graph_launches = e.launches;
-              e.used = ++g_graph_clock;
-              ++e.in_use;
-              break;
-            }
-        }
-        if (!gexec) {
-          cudaGraph_t graph;
-          const unsigned long long n0 = t_launches;
-          CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-          int rc = cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, true);
-          cudaError_t ce = cudaStreamEndCapture(st, &graph);
-          if (rc != LMG_OK) return rc;
-          if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-          graph_launches = t_launches - n0;
-          ce = cudaGraphInstantiate(&gexec, graph, 0);
-          cudaGraphDestroy(graph);
-          if (ce != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
-          g_launches -= graph_launches;  // counted per replay below
-          std::lock_guard<std::mutex> lk(g_graph_mu);
-          if (g_graphs.size() >= kGraphCacheSize) {  // evict the least recently used idle entry
-            size_t lru = g_graphs.size();
-            for (size_t i = 0; i < g_graphs.size(); ++i)
-              if (g_graphs[i].in_use == 0 && (lru == g_graphs.size() || g_graphs[i].used < g_graphs[lru].used))
-                lru = i;
-            if (lru < g_graphs.size()) {
-              cudaGraphExecDestroy(g_graphs[lru].exec);
-              g_graphs.erase(g_graphs.begin() + lru);
-            }
-          }
-          g_graphs.push_back(CycleGraph{key, gexec, graph_launches, ++g_graph_clock, 1});
-        }
-      }
-      CUDA_TRY(cudaGraphLaunch(gexec, st));
-      g_launches += graph_launches;
-    } else {
-      TRY(cycle(*fine, nlevels, 0, c, B, states, src, src_mode, ws, true, ws.norms, st, cyc > 0));
-    }
+    TRY(issue_cycle(cyc == 0));
     ++cyc;
     CUDA_TRY(cudaMemcpyAsync(nrm.data(), ws.norms, B * sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));

@@ -415,7 +415,8 @@ using Cfg16A = SwCfg<16, 1, 6, true, 16>;
 // with the reference's rounding.  Same chains, destinations and transient rows as sweep_kernel.
 constexpr int WST = 4;
 constexpr int WPB_MAX = 8;
-__host__ __device__ inline int wsweep_wpb(int B) { return B >= WPB_MAX ? WPB_MAX : B; }  // samples per CTA
+// samples (warps) per CTA: 1, 2, 4 or 8 (a compile-time copy split per CTA size)
+__host__ __device__ inline int wsweep_wpb(int B) { return B >= 5 ? 8 : B >= 3 ? 4 : B; }
 
 // one ring stage: W block (forward stored transposed, so both directions read [k][lane]), bias
 // row, the CTA's source rows and act' rows
@@ -425,11 +426,12 @@ struct WStage {
   static constexpr int SIZE = D + WPB_MAX * KM;  // doubles
 };
 
-// V (measurement knob LMG_WSWEEP_V): 0 = next stage's copies issued before the matvec; 1 = after
-// it (the LDGSTS then queue behind the matvec's LDS instead of ahead of them); 2 = 1 + the state
-// broadcast through shared memory (LDS.128 pairs) instead of 64-bit shuffles
-template <int KM, bool ADJ, int V = 1>
-__global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
+// V (measurement knob LMG_WSWEEP_V, 1 or 3): 1 = the next stage's copies issued after the
+// matvec; 3 = a quarter into its FMA chain (they fill its dependency stalls).  Measured and
+// dropped: 0 = before the matvec (the LDGSTS then queue ahead of its LDS), 2 = the state broadcast
+// through shared memory (LDS.128 pairs) instead of 64-bit shuffles (V == 2 code kept below)
+template <int KM, bool ADJ, int V = 1, int NW = WPB_MAX>
+__global__ void __launch_bounds__(32 * NW) wsweep_kernel(const SweepArgs a) {
   using SG = WStage<KM>;
   constexpr int QQ = KM * KM;
   extern __shared__ double wsm[];  // [64] double2 tanh table | [WST][SG::SIZE] ring | [8][KM] x
@@ -438,15 +440,16 @@ __global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
   double* xsh = ring + WST * SG::SIZE + (threadIdx.x >> 5) * KM;  // V 2: this warp's state row
   const int k = a.k0 + (int)blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = wsweep_wpb(a.B);  // samples per CTA (blockDim is always WPB_MAX warps)
+  constexpr int nw = NW;  // warps = samples per CTA
   const int b0 = (int)blockIdx.x * nw;
   const int b = b0 + warp;  // this warp's sample
   const int64_t BQ = (int64_t)a.B * KM;
   const Chain ch = chain_of(a, k, BQ);
   if (ch.nsteps <= 0) return;  // uniform over the CTA
-  const bool on = warp < nw && b < a.B && lane < KM;  // other warps still load and synchronise
+  const bool on = b < a.B && lane < KM;  // warps beyond the batch still load and synchronise
   const int li = lane & (KM - 1);
-  const int nthr = (int)blockDim.x, tid = (int)threadIdx.x;
+  constexpr int nthr = 32 * NW;
+  const int tid = (int)threadIdx.x;
   const int nwb = min(nw, a.B - b0) * KM;  // source / act' elements of this CTA's live samples
   const bool dense_src = a.src && !a.src_head;
   const bool has_b = !ADJ && a.bias;
@@ -467,15 +470,24 @@ __global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
   auto load_next = [&]() {  // everything step `loaded` reads -> slot loaded % WST
     if (loaded < ch.nsteps) {
       double* dst = ring + (loaded % WST) * SG::SIZE;
-      for (int e = tid; e < QQ; e += nthr) {
-        const int r = e / KM, cc = e % KM;  // W[r][cc]
-        cp_async<1>(dst + SG::W + (ADJ ? e : cc * KM + r), wl + e, true);
+#pragma unroll
+      for (int i = 0; i < (QQ + nthr - 1) / nthr; ++i) {  // straight-line copies (compile-time)
+        const int e = tid + i * nthr;
+        if (QQ % nthr == 0 || e < QQ) {
+          const int r = e / KM, cc = e % KM;  // W[r][cc]
+          cp_async<1>(dst + SG::W + (ADJ ? e : cc * KM + r), wl + e, true);
+        }
       }
       if (has_b && tid < KM) cp_async<1>(dst + SG::BIAS + tid, bl + tid, true);
-      if (dense_src)
-        for (int e = tid; e < nwb; e += nthr) cp_async<1>(dst + SG::SRC + e, sl + e, true);
-      if (ADJ && loaded + 1 < ch.nsteps)  // act' of row j scales the next step's operand
-        for (int e = tid; e < nwb; e += nthr) cp_async<1>(dst + SG::D + e, dl + e, true);
+#pragma unroll
+      for (int i = 0; i < (NW * KM + nthr - 1) / nthr; ++i) {
+        const int e = tid + i * nthr;
+        if (e < nwb) {
+          if (dense_src) cp_async<1>(dst + SG::SRC + e, sl + e, true);
+          if (ADJ && loaded + 1 < ch.nsteps)  // act' of row j scales the next step's operand
+            cp_async<1>(dst + SG::D + e, dl + e, true);
+        }
+      }
       wl += a.w_stride;
       if (has_b) bl += a.b_stride;
       if (dense_src) sl += BQ;
@@ -495,7 +507,17 @@ __global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
     if (a.write_row0) a.U[(int64_t)b * KM + lane] = x;  // states[0] = source[0]
   }
   const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0;
-  for (int s = 0; s < ch.nsteps; ++s) {
+  // destinations (dest_of) without per-step divisions: SW_SEQ and the U rows of a chain advance by
+  // one row per step; the C row, the P row and the advH row are fixed per chain
+  const int64_t bq = (int64_t)b * KM;
+  const bool fcf = a.mode == SW_FCF;
+  const int kc = fcf ? k * a.c : 0;
+  const int krow_end = fcf ? kc + a.c : 0;  // rows kc+1 .. kc+c-1 -> U, row (k+1)c -> P
+  double* const cptr = fcf ? ((k == a.n / a.c) ? a.halo : a.Cn + (int64_t)k * BQ) + bq : nullptr;
+  double* const pptr = fcf ? a.P + (int64_t)(k + 1) * BQ + bq : nullptr;
+  double* const aptr = (fcf && a.advH) ? a.advH + (int64_t)k * BQ + bq : nullptr;
+  double* urow = a.U + (int64_t)(ch.r0 + 1) * BQ + bq;
+  for (int s = 0; s < ch.nsteps; ++s, urow += BQ) {
     const int j = ch.r0 + 1 + s;  // row produced, with block j-1
     const bool last = s + 1 == ch.nsteps;
     if (tr) a.trace[4 * s] = clock64();
@@ -523,9 +545,10 @@ __global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
       for (int kk = 0; kk < KM; ++kk) {
         const double xk = __shfl_sync(0xffffffffu, xa, kk);
         acc = fma(st[SG::W + kk * KM + li], xk, acc);
+        if (V == 3 && kk == KM / 4) load_next();  // copies issued in the FMA chain's stalls
       }
     }
-    if (V != 0) load_next();
+    if (V == 1 || V == 2) load_next();
     if (tr) a.trace[4 * s + 2] = clock64();
     double pre = acc;
     if (has_b) pre = __dadd_rn(pre, bia);
@@ -534,10 +557,9 @@ __global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
     const double adv = __dadd_rn(x, __dmul_rn(a.h, v));
     const double o = __dadd_rn(dense_src ? sv : 0.0, adv);
     if (on) {
-      double* out = dest_of(a, k, j, BQ);
-      if (out) out[(int64_t)b * KM + lane] = o;
-      if (a.mode == SW_FCF && a.advH && j == k * a.c + 1)
-        a.advH[(int64_t)k * BQ + (int64_t)b * KM + lane] = __dadd_rn(x, __dmul_rn(a.h2, v));
+      double* out = !fcf ? urow : j < kc ? nullptr : j == kc ? cptr : j < krow_end ? urow : pptr;
+      if (out) out[lane] = o;
+      if (aptr && j == kc + 1) aptr[lane] = __dadd_rn(x, __dmul_rn(a.h2, v));
     }
     x = o;
     xa = ADJ ? __dmul_rn(o, dn) : o;
@@ -548,15 +570,15 @@ __global__ void __launch_bounds__(256) wsweep_kernel(const SweepArgs a) {
 template <int KM>
 size_t wsweep_smem() { return sizeof(double) * (128 + (size_t)WST * WStage<KM>::SIZE + WPB_MAX * KM); }
 
-// default 1 (tools/_r2_ws_ab.sh, profiles/r2_wsweep_variants.txt: serial propagation 2.77 vs
-// 3.05 / 3.08 ms at 4096 x 16 B 1 for variants 0 / 2; at 1024 x 32 B 64 variant 2 was faster
-// alone, 1.30 vs 1.42 ms, but slower in the c1 training step)
+// default 3 at q 16, 1 at q 32 (tools/_r2_ws_ab*.sh, profiles/r2_wsweep_variants.txt: serial
+// propagation at 4096 x 16 B 1: 2.77 (1) vs 3.05 / 3.08 ms (0 / 2), then 2.77 (3) vs 3.04 (1)
+// after the epilogue rework; at q 32 variant 3 slowed the c1 step 1.59 -> 2.23 ms)
 int wsweep_variant(int q) {
   static const int v = [] {
     const char* e = getenv("LMG_WSWEEP_V");
     return e ? atoi(e) : -1;
   }();
-  return v >= 0 ? v : 1;
+  return v >= 0 ? v : (q <= 16 ? 3 : 1);
 }
 
 
@@ -566,10 +588,10 @@ bool wsweep_enabled() {
   return !off;
 }
 
-template <int KM, bool ADJ, int V = 1>
+template <int KM, bool ADJ, int V = 1, int NW = WPB_MAX>
 cudaError_t wsweep_attr() {
   static const cudaError_t e = cudaFuncSetAttribute(
-      wsweep_kernel<KM, ADJ, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsweep_smem<KM>());
+      wsweep_kernel<KM, ADJ, V, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsweep_smem<KM>());
   return e;
 }
 
@@ -583,9 +605,9 @@ int wsweep_occupancy() {
   return per;
 }
 
-template <int KM, bool ADJ, int V>
+template <int KM, bool ADJ, int V, int NW>
 cudaError_t wlaunch_v(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
-  const cudaError_t e = wsweep_attr<KM, ADJ, V>();
+  const cudaError_t e = wsweep_attr<KM, ADJ, V, NW>();
   if (e != cudaSuccess) return e;
   static const bool pdl_on = getenv("LMG_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
@@ -598,16 +620,22 @@ cudaError_t wlaunch_v(const SweepArgs& a, const SweepShape& s, cudaStream_t st) 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_on ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, wsweep_kernel<KM, ADJ, V>, a);
+  return cudaLaunchKernelEx(&cfg, wsweep_kernel<KM, ADJ, V, NW>, a);
 }
 
 template <int KM, bool ADJ>
 cudaError_t wlaunch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
-  switch (wsweep_variant(KM)) {
-    case 0: return wlaunch_v<KM, ADJ, 0>(a, s, st);
-    case 2: return wlaunch_v<KM, ADJ, 2>(a, s, st);
-    default: return wlaunch_v<KM, ADJ, 1>(a, s, st);
-  }
+  auto by_nw = [&](auto vtag) {
+    constexpr int V = decltype(vtag)::value;
+    switch (s.nthreads / 32) {
+      case 1: return wlaunch_v<KM, ADJ, V, 1>(a, s, st);
+      case 2: return wlaunch_v<KM, ADJ, V, 2>(a, s, st);
+      case 4: return wlaunch_v<KM, ADJ, V, 4>(a, s, st);
+      default: return wlaunch_v<KM, ADJ, V, 8>(a, s, st);
+    }
+  };
+  return wsweep_variant(KM) == 3 ? by_nw(std::integral_constant<int, 3>{})
+                                 : by_nw(std::integral_constant<int, 1>{});
 }
 
 cudaError_t wsweep_launch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {
@@ -747,11 +775,9 @@ int sweep_shape(const SweepArgs& a, SweepShape* s, int forced_cfg) {
     const int wpb = wsweep_wpb(a.B);
     s->cfg = cfg;
     s->cs = 1;
-    // LMG_WSWEEP_FULLCTA=1: always 8 warps (the warps beyond the CTA's samples only share the
-    // ring copies) -- measured slower for one-sample chains (the 8-warp barrier per step costs
-    // more than the copies it spreads), so one warp per sample by default
-    static const bool full = getenv("LMG_WSWEEP_FULLCTA") != nullptr;
-    s->nthreads = 32 * (full ? WPB_MAX : wpb);
+    // one warp per sample (always-8-warp CTAs that only share the copies measured slower for
+    // one-sample chains: profiles/r2_wsweep_knobs.txt)
+    s->nthreads = 32 * wpb;
     s->smem = a.q <= 16 ? wsweep_smem<16>() : wsweep_smem<32>();
     s->grid = dim3(1, (a.B + wpb - 1) / wpb, nchains);
     return 0;
