@@ -1387,7 +1387,8 @@ int run_sweep(const SweepArgs& a, const SweepShape& sh, double steps, double wri
 
 // serial forward substitution as one persistent launch (one chain per 16-sample tile); -1 when
 // not eligible.  Only when all chains fit in one wave (otherwise the per-step path is faster).
-int seq_sweep(const lmg_system& S, int B, const double* src, int mode, double* U, cudaStream_t st) {
+int seq_sweep(const lmg_system& S, int B, const double* src, int mode, double* U, cudaStream_t st,
+              double* corrU = nullptr, int64_t corr_ts = 0, bool* corrected = nullptr) {
   if (S.num_layers < 2 || !sweep_basic_ok(S) || !aligned16(src) || !aligned16(U)) return -1;
   SweepArgs a = sweep_args(S, B, SW_SEQ, 1, src, mode, U);
   SweepShape sh;
@@ -1406,9 +1407,14 @@ int seq_sweep(const lmg_system& S, int B, const double* src, int mode, double* U
   }
   if ((int)sh.grid.y > sweep_clusters(S.width, a.adj, sh.cfg)) return -1;
   const int64_t BQ = (int64_t)B * S.width;
-  if (sh.cfg == SWEEP_CFG_WARP)
+  if (sh.cfg == SWEEP_CFG_WARP) {
     a.write_row0 = 1;  // the warp sweep stores states[0] itself (one launch fewer per solve)
-  else
+    if (corrU && corrected) {  // ... and applies the parent level's correction row by row
+      a.corrU = corrU;
+      a.corr_ts = corr_ts;
+      *corrected = true;
+    }
+  } else
     TRY(copy_rows(U, 0, src, 0, 1, BQ, st));  // states[0] = source[0]
   return run_sweep(a, sh, S.num_layers - 1, S.num_layers - 1, st);
 }
@@ -1442,8 +1448,10 @@ int fcf_sweep(const lmg_system& S, int B, int c, double* U, const double* src, i
     written += c + tail;
   }
   if (advH) written += nb;
-  TRY(run_sweep(a, sh, steps, written, st));
   const int64_t BQ = (int64_t)B * S.width;
+  // (a last-CTA-done commit inside the warp sweep instead of this launch measured much slower:
+  // one CTA then does the whole level's commit -- c7 3.70 vs 2.46 ms per step)
+  TRY(run_sweep(a, sh, steps, written, st));
   if (SH && advH)  // the commit and the level's coarse FAS source in one pass
     return launch(CLS_ELEM, 0.0, 48.0 * nb * BQ, st, [&] {
       ew_launch(k_commit_coarse, dim3(grid_for((int64_t)nb * BQ)), 256, st, U, src, Cn, advH, P, SH,
@@ -1532,9 +1540,10 @@ int local_fcf_fused(const lmg_system& S, int B, int c, double* U, const double* 
 // ------------------------------------------------------------------------------------------
 // reference routines
 
-int seq_forward(const lmg_system& S, int B, const double* src, int mode, double* U, cudaStream_t st) {
+int seq_forward(const lmg_system& S, int B, const double* src, int mode, double* U, cudaStream_t st,
+                double* corrU = nullptr, int64_t corr_ts = 0, bool* corrected = nullptr) {
   {
-    const int r = seq_sweep(S, B, src, mode, U, st);
+    const int r = seq_sweep(S, B, src, mode, U, st, corrU, corr_ts, corrected);
     if (r >= 0) return r;
   }
   const int64_t BQ = (int64_t)B * S.width;
@@ -1995,11 +2004,13 @@ int cycle(const lmg_system& S, int nlevels, int l, int c, int B, double* U, cons
   if (rs < 0)  // (the fused sweep assembled the coarse source with its commit)
     TRY(local_coarse_source(S, B, c, U, src, mode, P, nullptr, true, SH, coarsest ? nullptr : V, st,
                             ws.advH[l]));
+  bool corrected = false;  // the warp serial sweep applies this level's correction itself
   if (coarsest)
-    TRY(seq_forward(Sc, B, SH, LMG_SRC_DENSE, V, st));
+    TRY(seq_forward(Sc, B, SH, LMG_SRC_DENSE, V, st, want_norm ? nullptr : U,
+                    (int64_t)c * B * S.width, &corrected));
   else
     TRY(cycle(Sc, nlevels, l + 1, c, B, V, SH, LMG_SRC_DENSE, ws, false, nullptr, st));
-  if (!want_norm) TRY(local_correct(nb, B, S.width, c, U, V, st));
+  if (!want_norm && !corrected) TRY(local_correct(nb, B, S.width, c, U, V, st));
   if (want_norm) {  // correction fused into the C-row residual partials
     TRY(local_residual_post(S, B, c, U, src, mode, P, true, ws.block_part, ws.part,
                             l == 0 ? ws.Q : nullptr, st, V));

@@ -505,6 +505,11 @@ __global__ void __launch_bounds__(32 * NW) wsweep_kernel(const SweepArgs a) {
     x = ch.start[(int64_t)b * KM + lane];
     xa = ADJ ? __dmul_rn(x, a.D[(int64_t)ch.r0 * a.d_stride + (int64_t)b * KM + lane]) : x;
     if (a.write_row0) a.U[(int64_t)b * KM + lane] = x;  // states[0] = source[0]
+    if (a.corrU) {  // row 0's coarse-grid correction
+      double* cu = a.corrU + (int64_t)b * KM + lane;
+      const double u = *cu;
+      *cu = __dadd_rn(u, __dadd_rn(x, -u));
+    }
   }
   const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0;
   // destinations (dest_of) without per-step divisions: SW_SEQ and the U rows of a chain advance by
@@ -560,6 +565,11 @@ __global__ void __launch_bounds__(32 * NW) wsweep_kernel(const SweepArgs a) {
       double* out = !fcf ? urow : j < kc ? nullptr : j == kc ? cptr : j < krow_end ? urow : pptr;
       if (out) out[lane] = o;
       if (aptr && j == kc + 1) aptr[lane] = __dadd_rn(x, __dmul_rn(a.h2, v));
+      if (a.corrU) {  // SW_SEQ: the parent level's correction of row j (k_correct)
+        double* cu = a.corrU + (int64_t)j * a.corr_ts + bq + lane;
+        const double u = *cu;
+        *cu = __dadd_rn(u, __dadd_rn(o, -u));
+      }
     }
     x = o;
     xa = ADJ ? __dmul_rn(o, dn) : o;

@@ -55,6 +55,9 @@ struct SweepArgs {
   double* halo;
   int nchains;  // chains in this launch (0: all nb of the level)
   int write_row0;  // SW_SEQ, warp FMA sweep: also store U[0] = src[0] (the solve's first row)
+  // warp FMA sweep only, SW_SEQ: the parent level's coarse-grid correction of each produced row
+  // j, corrU[j*corr_ts] += row - corrU[j*corr_ts] (k_correct, same arithmetic)
+  double* corrU; int64_t corr_ts;
 };
 
 // warp-level FMA sweep for narrow networks (q <= 32; lmg_sweep.cu wsweep_kernel): no clusters,
