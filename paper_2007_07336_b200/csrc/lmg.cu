@@ -1793,6 +1793,27 @@ int local_residual_post(const lmg_system& S, int B, int c, const double* U, cons
   const int nt = row_slots(S);
   double* fpart = work;
   double* cpart = work + (size_t)nb * nt * B;
+  static const bool no_wresid = getenv("LMG_NO_WRESID") != nullptr;
+  if (Vcorr && is_first && (q == 16 || q == 32) && !is_conv(S) && !no_wresid && sweep_basic_ok(S)) {
+    // narrow networks: correction, C-row partials, kc+1 residual rows and block partials in one
+    // warp launch (same sums in the same order)
+    ResidArgs ra{};
+    ra.B = B; ra.q = q; ra.nb = nb; ra.c = c;
+    ra.adj = is_adjoint(S) ? 1 : 0;
+    ra.act = S.act; ra.is_first = 1; ra.h = S.step;
+    ra.W = S.W; ra.w_stride = S.w_stride;
+    ra.bias = ra.adj ? nullptr : S.b; ra.b_stride = S.b_stride;
+    ra.D = ra.adj ? S.D : nullptr; ra.d_stride = S.d_stride;
+    ra.src = src; ra.src_head = mode == LMG_SRC_HEAD;
+    ra.U = const_cast<double*>(U); ra.V = Vcorr; ra.P = P; ra.Q = Q; ra.block_part = block_part;
+    const double flops = (double)nb * B * (2.0 * q * q + 5.0 * q);
+    cudaError_t e = cudaSuccess;
+    route(LMG_ROUTE_WSWEEP);
+    TRY(launch(ra.adj ? CLS_SWEEP_ADJ : CLS_SWEEP_FWD, flops, 8.0 * nb * (q * q + 6.0 * B * q), st,
+               [&] { e = wresid_launch(ra, st); }));
+    if (e != cudaSuccess) return fail(LMG_ERR_CUDA, std::string("wresid launch: ") + cudaGetErrorString(e));
+    return LMG_OK;
+  }
   if (Vcorr)  // the correction U[kc] += V - U[kc] fused in (U is then written)
     TRY(launch(CLS_ELEM, 0.0, 32.0 * nb * BQ, st, [&] {
       ew_launch(k_correct_cpart, dim3(B, nb), 256, st, const_cast<double*>(U), Vcorr, P, src,

@@ -577,6 +577,99 @@ __global__ void __launch_bounds__(32 * NW) wsweep_kernel(const SweepArgs a) {
   }
 }
 
+template <int KM, bool ADJ, int NW>
+__global__ void __launch_bounds__(32 * NW) wresid_kernel(const ResidArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = (int)blockIdx.x * NW + warp, k = (int)blockIdx.y;
+  if (b >= a.B) return;  // no block-wide synchronisation below
+  const int q = KM;
+  const int64_t BQ = (int64_t)a.B * q, bq = (int64_t)b * q;
+  const bool on = lane < q;
+  const int li = lane & (KM - 1);
+  const int kc = k * a.c;
+  // 1. correction + C-row partial: k_correct_cpart (one 256-thread tree; lanes >= q hold 0.0)
+  double* urow = a.U + (int64_t)kc * BQ + bq;
+  double u1 = 0.0, rc = 0.0;
+  if (on) {
+    const double u0 = urow[lane];
+    u1 = __dadd_rn(u0, __dadd_rn(a.V[(int64_t)k * BQ + bq + lane], -u0));
+    urow[lane] = u1;
+    const double* p = (k == 0 && a.is_first) ? (a.src ? a.src + bq : nullptr) : a.P + (int64_t)k * BQ + bq;
+    const double r = __dadd_rn(p ? p[lane] : 0.0, -u1);
+    rc = fma(r, r, 0.0);
+  }
+#pragma unroll
+  for (int s2 = 16; s2 >= 1; s2 >>= 1) rc += __shfl_down_sync(0xffffffffu, rc, s2);
+  const double cpart = __shfl_sync(0xffffffffu, rc, 0);
+  // 2. row kc+1 = one layer step from the corrected U[kc] with block kc (E_RESID)
+  const double xa = ADJ ? __dmul_rn(u1, on ? a.D[(int64_t)kc * a.d_stride + bq + lane] : 0.0) : u1;
+  const double* Wb = a.W + (int64_t)kc * a.w_stride;
+  double acc = 0.0;
+#pragma unroll
+  for (int kk = 0; kk < KM; ++kk) {
+    const double xk = __shfl_sync(0xffffffffu, xa, kk);
+    acc = fma(ADJ ? Wb[kk * q + li] : Wb[li * q + kk], xk, acc);
+  }
+  double pre = acc;
+  if (!ADJ && a.bias) pre = __dadd_rn(pre, a.bias[(int64_t)kc * a.b_stride + li]);
+  const double v = ADJ ? pre : act_fwd(a.act, pre);
+  const double adv = __dadd_rn(u1, __dmul_rn(a.h, v));
+  const double sv = (a.src && !a.src_head && on) ? a.src[(int64_t)(kc + 1) * BQ + bq + lane] : 0.0;
+  const double prop = __dadd_rn(sv, adv);
+  double r = 0.0;
+  if (on) {
+    r = __dadd_rn(prop, -urow[BQ + lane]);
+    if (a.Q) a.Q[(int64_t)k * BQ + bq + lane] = prop;
+  }
+  // E_RESID row partial: per 16-column warp of the 32-column tile, lane fk accumulates columns
+  // 2fk, 2fk+1, 8+2fk, 9+2fk (fma, in that order), then a shfl-xor 1 / 2 tree, then the warps
+  // in order from 0.0
+  const int g = (lane >> 2) & 1, fk = lane & 3;  // lanes 0..7: (warp g, lane fk)
+  double vsum = 0.0;
+#pragma unroll
+  for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int n = 16 * g + 8 * jj + 2 * fk + e;
+      const double rn = __shfl_sync(0xffffffffu, r, n & 31);
+      if (n < q && lane < 8) vsum = fma(rn, rn, vsum);
+    }
+  vsum += __shfl_xor_sync(0xffffffffu, vsum, 1);
+  vsum += __shfl_xor_sync(0xffffffffu, vsum, 2);
+  const double w0 = __shfl_sync(0xffffffffu, vsum, 0), w1 = __shfl_sync(0xffffffffu, vsum, 4);
+  double fpart = 0.0;
+  fpart += w0;
+  fpart += w1;
+  // 3. block partial (k_combine_post: cpart, then the tile partials)
+  if (lane == 0) {
+    double s3 = cpart;
+    s3 += fpart;
+    a.block_part[(int64_t)k * a.B + b] = s3;
+  }
+}
+
+template <int KM, bool ADJ>
+cudaError_t wresid_launch_t(const ResidArgs& a, cudaStream_t st) {
+  const int nw = wsweep_wpb(a.B);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.B + nw - 1) / nw, a.nb, 1);
+  cfg.blockDim = dim3(32 * nw, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = getenv("LMG_NO_PDL") ? 0 : 1;
+  switch (nw) {
+    case 1: return cudaLaunchKernelEx(&cfg, wresid_kernel<KM, ADJ, 1>, a);
+    case 2: return cudaLaunchKernelEx(&cfg, wresid_kernel<KM, ADJ, 2>, a);
+    case 4: return cudaLaunchKernelEx(&cfg, wresid_kernel<KM, ADJ, 4>, a);
+    default: return cudaLaunchKernelEx(&cfg, wresid_kernel<KM, ADJ, 8>, a);
+  }
+}
+
 template <int KM>
 size_t wsweep_smem() { return sizeof(double) * (128 + (size_t)WST * WStage<KM>::SIZE + WPB_MAX * KM); }
 
@@ -808,6 +901,12 @@ int sweep_shape(const SweepArgs& a, SweepShape* s, int forced_cfg) {
   });
   s->grid = dim3(s->cs, mt, nchains);
   return 0;
+}
+
+cudaError_t wresid_launch(const ResidArgs& a, cudaStream_t st) {
+  if (a.q == 16) return a.adj ? wresid_launch_t<16, true>(a, st) : wresid_launch_t<16, false>(a, st);
+  if (a.q == 32) return a.adj ? wresid_launch_t<32, true>(a, st) : wresid_launch_t<32, false>(a, st);
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t sweep_launch(const SweepArgs& a, const SweepShape& s, cudaStream_t st) {

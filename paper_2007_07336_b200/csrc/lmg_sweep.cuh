@@ -63,6 +63,26 @@ struct SweepArgs {
 // warp-level FMA sweep for narrow networks (q <= 32; lmg_sweep.cu wsweep_kernel): no clusters,
 // grid (1, batch groups of 8 samples, chains)
 constexpr int SWEEP_CFG_WARP = 4;
+// Post-correction residual of a narrow level (q 16 / 32) in one launch (lmg_sweep.cu
+// wresid_kernel): the correction U[kc] += V[k] - U[kc] with its C-row residual partial
+// (k_correct_cpart), the kc+1 residual rows as one warp FMA step each (E_RESID, propagated rows
+// -> Q) and the per-block partials (k_combine_post) -- every sum in the order those kernels use,
+// so the block partials, and the norms, are bitwise theirs.
+struct ResidArgs {
+  int B, q, nb, c, adj, act, is_first;
+  double h;
+  const double* W; int64_t w_stride;
+  const double* bias; int64_t b_stride;
+  const double* D; int64_t d_stride;
+  const double* src; int src_head;  // level source (head: only row 0)
+  double* U;
+  const double* V;  // coarse-grid solution rows (the correction)
+  const double* P;  // propagated C rows
+  double* Q;        // optional: propagated rows kc+1
+  double* block_part;
+};
+cudaError_t wresid_launch(const ResidArgs& a, cudaStream_t st);
+
 // configuration the launcher would use for (q, B, adj), or -1 if the fused sweep cannot run it
 int sweep_config(int q, int B, int adj, int nclusters_hint);
 // dynamic shared memory, cluster size and grid of a config
