@@ -591,9 +591,15 @@ def run_ours(args, cfg):
                           tflops=(s_flops / (s_ms * 1e-3) / 1e12) if s_ms else None,
                           share_of_step=(s_ms / (inst_ms * args.steps)) if inst_ms else None),
                       fused_sweeps=dict(
-                          what="fused persistent FCF / serial sweeps (state on chip)",
+                          what="fused persistent FCF / serial sweeps (state on chip; for q 16 / 32 "
+                               "the warp-level FMA sweeps, state in registers)",
                           ms_per_step=w_ms / args.steps, launches_per_step=w_n / args.steps,
-                          gbs=(w_bytes / (w_ms * 1e-3) / 1e9) if w_ms else None),
+                          gbs=(w_bytes / (w_ms * 1e-3) / 1e9) if w_ms else None,
+                          share_of_step=(w_ms / (inst_ms * args.steps)) if inst_ms else None,
+                          bound=("latency: a serial chain of dependent layer steps; the warp FMA "
+                                 "sweep runs 992 SM cycles per step against a ~450-cycle "
+                                 "dependency floor (profiles/r2_ncu_wsweep.json, DESIGN 3)")
+                          if cfg.get("width", 0) in (16, 32) else None),
                       all_step_gemm_tflops=((gemm_flops + s_flops) / ((gemm_ms + s_ms) * 1e-3) / 1e12)
                       if gemm_ms + s_ms > 0 else None,
                       launches=f_n + a_n, all_kernel_ms_per_step=all_ms / args.steps,

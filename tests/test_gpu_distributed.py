@@ -26,6 +26,8 @@ import torch.distributed as dist  # noqa: E402
 import torch.multiprocessing as mp  # noqa: E402
 
 N, Q, B, C, THR = 256, 64, 8, 4, 16  # levels [256, 64, 16]
+# the spawned workers of the narrow-network case read their width from the environment
+Q = int(os.environ.get("LMG_TEST_Q", Q))
 SHAPE = (N, C, THR)
 # cf 16, levels [256, 16, 1]: at 8 ranks level 1 does not split into whole blocks, so [16, 1] is
 # gathered onto every rank (distributed.check_partition) -- the c5 hierarchy's situation at 8 GPUs
@@ -226,6 +228,22 @@ def test_collapsed_coarse_levels_bitwise_at_eight_ranks(tmp_path):
     ref = _spawn(_single, (str(tmp_path / "c16.pkl"), SHAPE_C16), 1, str(tmp_path / "c16.pkl"), env)
     for world in (2, 8):
         r = _run(world, tmp_path, env, SHAPE_C16)
+        assert r["U"].tobytes() == ref["U"].tobytes(), world
+        assert np.array_equal(r["hist"], ref["hist"][: ref["cyc"].max() + 1], equal_nan=True), world
+        assert np.array_equal(r["ahist"], ref["ahist"][: ref["acyc"].max() + 1], equal_nan=True), world
+        assert r["W"].tobytes() == ref["W"].tobytes(), world
+        assert np.array_equal(r["loss"], ref["loss"]), world
+
+
+def test_partitioned_warp_sweeps_bitwise(tmp_path):
+    """Narrow network (q 16): every rank's relaxed level runs the warp-level FMA sweeps (halo chain,
+    exchange, block 0) and the single GPU runs them with the fused commit / residual launches --
+    states, histories and updated parameters are BITWISE identical for world 1, 2 and 4."""
+    env = {"LMG_TEST_Q": "16", "LMG_NO_SPLITK": "1"}
+    ref = _spawn(_single, (str(tmp_path / "q16.pkl"),), 1, str(tmp_path / "q16.pkl"), env)
+    for world in (1, 2, 4):
+        r = _run(world, tmp_path, env)
+        assert r["fused"], world  # the partitioned levels really ran lmg_local_fcf_fused
         assert r["U"].tobytes() == ref["U"].tobytes(), world
         assert np.array_equal(r["hist"], ref["hist"][: ref["cyc"].max() + 1], equal_nan=True), world
         assert np.array_equal(r["ahist"], ref["ahist"][: ref["acyc"].max() + 1], equal_nan=True), world
