@@ -202,15 +202,31 @@ __global__ void k_resid_row0_tiles(const double* __restrict__ S0, const double* 
   part[b] = rs;
 }
 
-// norms[b] = sqrt(sum over slots, in slot order) -- deterministic for any launch geometry
+// norms[b] = sqrt(sum over slots, in slot order) -- deterministic for any launch geometry.  One
+// warp per sample: the lanes fetch a chunk of 256 slots at once into shared memory (one memory
+// latency per chunk instead of a dependent load per slot), then lane 0 adds them in slot order.
+constexpr int kNormChunk = 256;
 __global__ void k_reduce_norms(const double* __restrict__ part, int64_t nslots, int B,
                                double* __restrict__ norms) {
   pdl_enter();
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
+  __shared__ double buf[4][kNormChunk];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 4 + w;
+  if (b >= B) return;  // whole warps
   double s = 0.0;
-  for (int64_t k = 0; k < nslots; ++k) s += part[k * B + b];
-  norms[b] = sqrt(s);
+  for (int64_t k0 = 0; k0 < nslots; k0 += kNormChunk) {
+    const int n = nslots - k0 < kNormChunk ? (int)(nslots - k0) : kNormChunk;
+#pragma unroll
+    for (int i = 0; i < kNormChunk / 32; ++i) {
+      const int kk = lane + 32 * i;
+      if (kk < n) buf[w][kk] = part[(k0 + kk) * B + b];
+    }
+    __syncwarp();
+    if (lane == 0)
+      for (int kk = 0; kk < n; ++kk) s += buf[w][kk];
+    __syncwarp();
+  }
+  if (lane == 0) norms[b] = sqrt(s);
 }
 
 // bias gradient + SGD: gb_n[i] = (h * sum_b lam^{n+1}[b,i] D_n[b,i]) * scale ; b_n -= lr*gb_n
@@ -1917,7 +1933,7 @@ int residual_full(const lmg_system& S, int B, const double* U, const double* src
 }
 
 int reduce_norms(const double* part, int64_t nslots, int B, double* norms, cudaStream_t st) {
-  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { ew_launch(k_reduce_norms, dim3((B + 127) / 128), 128, st, part, nslots, B, norms); }));
+  TRY(launch(CLS_ELEM, 0.0, 0.0, st, [&] { ew_launch(k_reduce_norms, dim3((B + 3) / 4), 128, st, part, nslots, B, norms); }));
   return LMG_OK;
 }
 
@@ -1984,7 +2000,7 @@ int layout_ws(const lmg_system& fine, int nlevels, int c, int B, char* base, Wor
 
 int norms_from_blocks(const double* block_part, int nblocks, int B, double* norms, cudaStream_t st) {
   return launch(CLS_ELEM, 0.0, 0.0, st, [&] {
-    ew_launch(k_reduce_norms, dim3((B + 127) / 128), 128, st, block_part, nblocks, B, norms);
+    ew_launch(k_reduce_norms, dim3((B + 3) / 4), 128, st, block_part, nblocks, B, norms);
   });
 }
 

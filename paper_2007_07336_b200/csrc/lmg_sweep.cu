@@ -530,6 +530,10 @@ __global__ void __launch_bounds__(32 * NW) wsweep_kernel(const SweepArgs a) {
     __syncthreads();     // ... and everyone's; every warp is done with slot (s-1) % WST
     if (tr) a.trace[4 * s + 1] = clock64();
     if (V == 0) load_next();
+    // SW_SEQ correction of this step's row: its old value is loaded now, used after the epilogue
+    // (a load consumed in the same step would stall the warp's in-order issue for its latency)
+    double* cu = (a.corrU && on) ? a.corrU + (int64_t)j * a.corr_ts + bq + lane : nullptr;
+    const double cu_old = cu ? *cu : 0.0;
     const double* st = ring + (s % WST) * SG::SIZE;
     const double bia = has_b ? st[SG::BIAS + li] : 0.0;
     const double sv = dense_src ? st[SG::SRC + warp * KM + li] : 0.0;
@@ -565,11 +569,7 @@ __global__ void __launch_bounds__(32 * NW) wsweep_kernel(const SweepArgs a) {
       double* out = !fcf ? urow : j < kc ? nullptr : j == kc ? cptr : j < krow_end ? urow : pptr;
       if (out) out[lane] = o;
       if (aptr && j == kc + 1) aptr[lane] = __dadd_rn(x, __dmul_rn(a.h2, v));
-      if (a.corrU) {  // SW_SEQ: the parent level's correction of row j (k_correct)
-        double* cu = a.corrU + (int64_t)j * a.corr_ts + bq + lane;
-        const double u = *cu;
-        *cu = __dadd_rn(u, __dadd_rn(o, -u));
-      }
+      if (cu) *cu = __dadd_rn(cu_old, __dadd_rn(o, -cu_old));  // SW_SEQ: k_correct of row j
     }
     x = o;
     xa = ADJ ? __dmul_rn(o, dn) : o;
