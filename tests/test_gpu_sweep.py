@@ -124,3 +124,19 @@ def test_chain_launch_is_bitwise_the_per_step_path(case, tmp_path):
         assert ch["routes"][ROUTES.index("chain")] > 0, tile
         for key in ("U0", "hist", "cyc", "U1", "lam", "loss", "adj_hist", "adj_cyc", "W", "b", "Us"):
             assert np.array_equal(ch[key], per_step[key], equal_nan=True), (tile, key)
+
+
+@pytest.mark.parametrize("case", [(256, 16, 3, 4, 16), (64, 32, 9, 4, 4)],
+                         ids=lambda c: "N%d_q%d_B%d_c%d" % c[:4])
+def test_warp_sweep_repeatable(case, tmp_path):
+    """The warp FMA sweeps' cp.async ring (slot reuse one step after its last read, behind the
+    step's barrier) and the fused narrow residual: two runs of a whole training step are bitwise
+    identical, with partial CTAs (3 samples on a 4-warp CTA; 9 = 8 + 1) -- compute-sanitizer is
+    closed on this GPU pool, so a repeat test stands in for racecheck here."""
+    from paper_2007_07336_b200._lib import ROUTES
+
+    a = _run(case, tmp_path, {"LMG_NO_SPLITK": "1"})
+    b = _run(case, tmp_path, {"LMG_NO_SPLITK": "1", "LMG_REPEAT_TAG": "2"})
+    assert a["routes"][ROUTES.index("wsweep")] > 0
+    for key in ("U0", "hist", "cyc", "U1", "lam", "loss", "adj_hist", "adj_cyc", "W", "b", "Us"):
+        assert np.array_equal(a[key], b[key], equal_nan=True), key

@@ -14,6 +14,9 @@ Cases (and the kernels they route to, asserted through lmg_route_counts):
                                          LMG_NO_SWEEP=1
   chain   N 64, q 128, B 16, cf 4     -- persistent chain launches (completion counters,
                                          cooperative grid); LMG_NO_SWEEP=1
+  warp16  N 256, q 16, B 3, cf 4, levels [256, 64, 16] -- warp FMA sweeps (cp.async ring, 4-warp
+                                         CTAs with an idle warp) + the fused narrow residual
+  warp32  N 64, q 32, B 9, cf 4       -- the same at q 32, two CTAs per chain (8 + 1 samples)
 """
 
 import os
@@ -31,7 +34,9 @@ from paper_2007_07336_b200 import _lib  # noqa: E402
 CASES = {"tgemm": (16, 128, 64, 4, 4, ("tgemm_big",)),
          "sweep": (64, 128, 16, 4, 4, ("sweep_fcf", "sweep_seq")),
          "splitk": (16, 128, 32, 4, 4, ("serial_splitk",)),
-         "chain": (64, 128, 16, 4, 4, ("chain",))}
+         "chain": (64, 128, 16, 4, 4, ("chain",)),
+         "warp16": (256, 16, 3, 4, 16, ("wsweep", "sweep_fcf", "sweep_seq")),
+         "warp32": (64, 32, 9, 4, 4, ("wsweep", "sweep_fcf", "sweep_seq"))}
 
 
 def main():
