@@ -103,8 +103,9 @@ def trace(N=None, q=None, B=None):
     main = np.median(t[1:, 2] - t[1:, 1])
     epi = np.median(t[1:, 3] - t[1:, 2])
     step = np.median(np.diff(t[:, 0]))
-    print(f"serial trace (ns, median per step): step {step:.0f} = wait-for-peers {wait:.0f} + "
-          f"mainloop {main:.0f} + epilogue {epi:.0f} + push/rest {step - wait - main - epi:.0f}")
+    unit = "SM cycles" if q in (16, 32) else "ns"  # the warp FMA sweep stamps clock64
+    print(f"serial trace ({unit}, median per step): step {step:.0f} = wait {wait:.0f} + "
+          f"mainloop {main:.0f} + epilogue {epi:.0f} + rest {step - wait - main - epi:.0f}")
 
 
 if __name__ == "__main__" and os.environ.get("LMG_TRACE"):
