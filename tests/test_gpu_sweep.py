@@ -35,6 +35,8 @@ CASES = [
     (64, 256, 16, 4, 0, "identity"),
     (64, 16, 4, 4, 0),       # 16-column shape (q = 16): one CTA per chain
     (256, 16, 1, 16, 4),     # c6-shaped: q 16, one sample, cf 16, levels [256, 16, 1]
+    (64, 32, 160, 4, 16),    # q 32, B 160: per-step FCF (B > 64), warp serial sweeps and the fused
+                             # narrow residual over 20 eight-warp CTAs per block
 ]
 
 
