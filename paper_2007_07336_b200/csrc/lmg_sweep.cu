@@ -429,15 +429,14 @@ struct WStage {
 // V (measurement knob LMG_WSWEEP_V, 1 or 3): 1 = the next stage's copies issued after the
 // matvec; 3 = a quarter into its FMA chain (they fill its dependency stalls).  Measured and
 // dropped: 0 = before the matvec (the LDGSTS then queue ahead of its LDS), 2 = the state broadcast
-// through shared memory (LDS.128 pairs) instead of 64-bit shuffles (V == 2 code kept below)
+// through shared memory (LDS.128 pairs) instead of 64-bit shuffles (profiles/r2_wsweep_*)
 template <int KM, bool ADJ, int V = 1, int NW = WPB_MAX>
 __global__ void __launch_bounds__(32 * NW) wsweep_kernel(const SweepArgs a) {
   using SG = WStage<KM>;
   constexpr int QQ = KM * KM;
-  extern __shared__ double wsm[];  // [64] double2 tanh table | [WST][SG::SIZE] ring | [8][KM] x
+  extern __shared__ double wsm[];  // [64] double2 tanh table | [WST][SG::SIZE] ring
   double2* tab = reinterpret_cast<double2*>(wsm);
   double* ring = wsm + 128;
-  double* xsh = ring + WST * SG::SIZE + (threadIdx.x >> 5) * KM;  // V 2: this warp's state row
   const int k = a.k0 + (int)blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int nw = NW;  // warps = samples per CTA
@@ -529,7 +528,6 @@ __global__ void __launch_bounds__(32 * NW) wsweep_kernel(const SweepArgs a) {
     cp_wait<WST - 2>();  // this thread's copies of stage s landed
     __syncthreads();     // ... and everyone's; every warp is done with slot (s-1) % WST
     if (tr) a.trace[4 * s + 1] = clock64();
-    if (V == 0) load_next();
     // SW_SEQ correction of this step's row: its old value is loaded now, used after the epilogue
     // (a load consumed in the same step would stall the warp's in-order issue for its latency)
     double* cu = (a.corrU && on) ? a.corrU + (int64_t)j * a.corr_ts + bq + lane : nullptr;
@@ -539,25 +537,13 @@ __global__ void __launch_bounds__(32 * NW) wsweep_kernel(const SweepArgs a) {
     const double sv = dense_src ? st[SG::SRC + warp * KM + li] : 0.0;
     const double dn = (ADJ && !last) ? st[SG::D + warp * KM + li] : 0.0;
     double acc = 0.0;
-    if (V == 2) {
-      if (lane < KM) xsh[lane] = xa;
-      __syncwarp();
 #pragma unroll
-      for (int kk = 0; kk < KM; kk += 2) {
-        const double2 xk = *reinterpret_cast<const double2*>(xsh + kk);
-        acc = fma(st[SG::W + kk * KM + li], xk.x, acc);
-        acc = fma(st[SG::W + (kk + 1) * KM + li], xk.y, acc);
-      }
-      __syncwarp();  // the next step's store must not overtake a lagging lane's reads
-    } else {
-#pragma unroll
-      for (int kk = 0; kk < KM; ++kk) {
-        const double xk = __shfl_sync(0xffffffffu, xa, kk);
-        acc = fma(st[SG::W + kk * KM + li], xk, acc);
-        if (V == 3 && kk == KM / 4) load_next();  // copies issued in the FMA chain's stalls
-      }
+    for (int kk = 0; kk < KM; ++kk) {
+      const double xk = __shfl_sync(0xffffffffu, xa, kk);
+      acc = fma(st[SG::W + kk * KM + li], xk, acc);
+      if (V == 3 && kk == KM / 4) load_next();  // copies issued in the FMA chain's stalls
     }
-    if (V == 1 || V == 2) load_next();
+    if (V == 1) load_next();
     if (tr) a.trace[4 * s + 2] = clock64();
     double pre = acc;
     if (has_b) pre = __dadd_rn(pre, bia);
@@ -671,7 +657,7 @@ cudaError_t wresid_launch_t(const ResidArgs& a, cudaStream_t st) {
 }
 
 template <int KM>
-size_t wsweep_smem() { return sizeof(double) * (128 + (size_t)WST * WStage<KM>::SIZE + WPB_MAX * KM); }
+size_t wsweep_smem() { return sizeof(double) * (128 + (size_t)WST * WStage<KM>::SIZE); }
 
 // default 3 at q 16, 1 at q 32 (tools/_r2_ws_ab*.sh, profiles/r2_wsweep_variants.txt: serial
 // propagation at 4096 x 16 B 1: 2.77 (1) vs 3.05 / 3.08 ms (0 / 2), then 2.77 (3) vs 3.04 (1)
