@@ -97,7 +97,7 @@ enum {
   LMG_ROUTE_CONV_ADJ = 12,       /* conv2d adjoint step                                 */
   LMG_ROUTE_CONV_PGRAD = 13,     /* conv2d parameter gradients                          */
   LMG_ROUTE_CHAIN = 14,          /* persistent chain launch of a whole relaxation sweep  */
-  LMG_ROUTE_WSWEEP = 15,         /* warp-level FMA sweep (q <= 32), FCF or serial        */
+  LMG_ROUTE_WSWEEP = 15,         /* warp-level FMA sweep (q 16/32, FCF or serial) or the fused narrow residual */
   LMG_ROUTE_N = 16
 };
 int lmg_route_counts(unsigned long long* out, int n);
